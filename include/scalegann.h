@@ -1,0 +1,243 @@
+/*
+ * scalegann.h — C ABI of libscalegann.so, the B200 (sm_100a) hot path of
+ * ScaleGANN's divide-and-merge graph-index construction (arxiv 2605.10135).
+ *
+ * "P:n" cites /root/reference/PAPER.md line n; "S:n" cites SPEC.md; "R<n>" is
+ * a numbered reading of the paper in DESIGN.md ("Readings").
+ *
+ * Conventions (all functions):
+ *  - Plain C: no C++ types, no exceptions, no torch types.  `stream` is a
+ *    cudaStream_t passed as void* (NULL = legacy default stream).
+ *  - Every pointer named x, home, idmap, graph, ... is DEVICE memory on the
+ *    current CUDA device unless its name ends in `_host`.  Buffers are owned by
+ *    the caller; the library never frees caller memory and allocates nothing:
+ *    scratch comes from the caller's `ws` (device) of `ws_bytes`, sized by the
+ *    matching *_workspace() query.  Too small a workspace -> SG_ERR_WORKSPACE.
+ *  - Calls are stream-ordered and asynchronous except those with a `_host`
+ *    output, which synchronise `stream` before returning.
+ *  - Arguments are validated before any launch; on error nothing is launched
+ *    (or, for errors found on the device, outputs are unspecified) and
+ *    scalegann_last_error() returns a thread-local message.  CUDA errors map to
+ *    SG_ERR_CUDA; asynchronous kernel faults surface at the next synchronising
+ *    call.
+ *  - Rows are row-major; ids are uint32 with SG_SENTINEL (0xFFFFFFFF)
+ *    for "none"; vector data is n x d of SG_U8 or SG_F32 (paper Table
+ *    tab:dataset).
+ *  - Local ids of a shard index its idmap, which is ascending in global id
+ *    (reading R8), so every (dist, id) tie-break agrees across shards.
+ */
+#ifndef SCALEGANN_H
+#define SCALEGANN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SCALEGANN_ABI_VERSION 1
+#define SG_SENTINEL 0xFFFFFFFFu
+
+typedef enum {
+    SG_OK = 0,
+    SG_ERR_INVALID_ARG = 1,
+    SG_ERR_UNSUPPORTED = 2,
+    SG_ERR_CUDA = 3,
+    SG_ERR_CAPACITY = 4,    /* a primary found every cluster full */
+    SG_ERR_WORKSPACE = 5,   /* ws_bytes smaller than the *_workspace() answer */
+    SG_ERR_TOO_SMALL = 6    /* shard with m < 2 */
+} sg_status;
+
+typedef enum { SG_U8 = 0, SG_F32 = 1 } sg_dtype;
+typedef enum { SG_L2 = 0, SG_IP = 1 } sg_metric;   /* squared L2 / negative inner product (R2) */
+
+/* Operand precision of the distance GEMM; accumulation is always fp32 (R3). */
+typedef enum {
+    SG_PREC_AUTO = 0,       /* F16_EXACT when exact (u8, or integral f32 with the bound below), else TF32 */
+    SG_PREC_F16_EXACT = 1,  /* kind::f16; exact when all values are integers |v| <= 2048 and 2*d*max^2 < 2^24 */
+    SG_PREC_TF32 = 2,       /* kind::tf32, operands rounded to tf32 (RN) */
+    SG_PREC_TF32X3 = 3      /* kind::tf32 on [hi|hi|lo].[hi|lo|hi]: ~fp32-accurate products */
+} sg_precision;
+
+/* Alg. 1 inputs + the paper-gap decisions of readings R4-R9. */
+typedef struct {
+    uint32_t k;            /* clusters = shards */
+    uint32_t omega;        /* max homes per vector incl. the primary */
+    float epsilon;         /* selectivity eps, default 1.2 */
+    uint32_t theta0_ppm;   /* base replica fraction theta0 in ppm (R4), default 400000 */
+    float alpha;           /* tau_b = 1 + alpha/(1+b) (R5), default 1.0 */
+    uint32_t block_size;   /* vectors per block, default 65536 */
+    uint64_t capacity;     /* max vectors per cluster; 0 = derive (R9) */
+} sg_partition_params;
+
+typedef struct {
+    uint32_t L;               /* intermediate kNN degree, <= 256 */
+    uint32_t R;               /* final out-degree, R <= L, R <= 128 */
+    int32_t metric;           /* sg_metric */
+    int32_t precision;        /* sg_precision */
+    uint32_t prune_rule;      /* 0 = rule P (R10), 1 = relaxed */
+    uint32_t protected_edges; /* h forward edges kept by reverse insertion; 0 = R/2 (R11) */
+} sg_build_params;
+
+int scalegann_abi_version(void);
+const char* scalegann_last_error(void);
+
+/* ---- a1: centroids (reading R0) ----------------------------
+ * k-means++ seeding + Lloyd on the strided sample floor(i*n/S), S =
+ * min(n, spc*k), seeds drawn from splitmix64(seed).  Writes k x d float32
+ * centroids (device).  Not bit-exact with the oracle: accepted when its sample
+ * distortion is <= 1.01 x the oracle's.  Requires k <= 64, d <= 1024. */
+sg_status scalegann_kmeans_workspace(uint64_t n, uint32_t d, uint32_t k, uint32_t spc, size_t* bytes);
+sg_status scalegann_kmeans(const void* x, sg_dtype dtype, uint64_t n, uint32_t d, uint32_t k,
+                           uint64_t seed, uint32_t max_iter, uint32_t spc, float* centroids,
+                           void* ws, size_t ws_bytes, void* stream);
+
+/* ---- a2-a3: overlapping balanced partition (Alg. 1) --
+ * For every vector v: d^2(v,c) to all centroids in the fixed fp32 fmaf order of
+ * R1, then block by block (block_size vectors in id order): primaries to
+ * the nearest cluster with size < capacity, statistics/thresholds
+ * (R4, R5), replicas per Algorithm 1 with checkSizeLimit = R7.  Bit-exact with
+ * the oracle.
+ *   x          n x d vectors (device)
+ *   centroids  k x d float32 (device)
+ *   home       out, n x omega uint32: [primary, replicas in placement order, SENTINEL...]
+ *   primary_d  out, n float32: d^2(v, primary)
+ *   counts_host out (host), 3*k uint64: sizes[k], primaries[k], replicas[k]; synchronises
+ * Errors: SG_ERR_INVALID_ARG (k == 0 or > 64, omega == 0 or > k, eps <= 0,
+ * theta0_ppm not in (0, 1e6), capacity*k < n, block_size == 0), SG_ERR_CAPACITY. */
+sg_status scalegann_partition_workspace(uint64_t n, uint32_t d, const sg_partition_params* p, size_t* bytes);
+sg_status scalegann_partition(const void* x, sg_dtype dtype, uint64_t n, uint32_t d,
+                              const float* centroids, const sg_partition_params* p, uint32_t* home,
+                              float* primary_d, uint64_t* counts_host, void* ws, size_t ws_bytes,
+                              void* stream);
+
+/* ---- a4: shard membership (R8) --------------------------------------------
+ * idmap = ascending global ids v with `shard` in home[v] (m entries, caller
+ * sized from counts_host).  inv (optional, n x omega, device): for each (v, h)
+ * with home[v*omega+h] == shard, inv[v*omega+h] = local id of v in the shard;
+ * other entries untouched.  m_host (optional) receives m and synchronises. */
+sg_status scalegann_shard_idmap_workspace(uint64_t n, size_t* bytes);
+sg_status scalegann_shard_idmap(const uint32_t* home, uint64_t n, uint32_t omega, uint32_t shard,
+                                uint32_t* idmap, uint32_t* inv, uint64_t* m_host, void* ws,
+                                size_t ws_bytes, void* stream);
+
+/* ---- entry points (reading R13) ---------------------------------------------
+ * entry_host[s] = argmin over primaries of shard s of (primary_d, gid), or
+ * SENTINEL; returns the global entry (largest shard's entry, ties to lower s)
+ * in *global_entry_host.  Synchronises. */
+sg_status scalegann_entry_points(const uint32_t* home, const float* primary_d, uint64_t n,
+                                 uint32_t omega, uint32_t k, const uint64_t* sizes_host,
+                                 uint32_t* entry_host, uint32_t* global_entry_host, void* ws,
+                                 size_t ws_bytes, void* stream);
+
+/* ---- a5: exact kNN (north_star stage 2; R2, R3) ---------------------------
+ * For each row i of A (rows ida[0..ma) of xa, or 0..ma-1 if ida == NULL): the L
+ * smallest (dist, j) over rows j of B (idb / xb likewise), j != i when
+ * self_exclude (A and B the same set).  dist = |a|^2 + |b|^2 - 2 a.b (L2) or
+ * -a.b (IP), distance tiles on tcgen05 tensor cores with fp32 accumulation and
+ * a fused per-row top-L.  ids/dists out: ma x L, rows sorted by (dist, id),
+ * padded with (SENTINEL, +inf) when fewer than L candidates exist.
+ * Limits: L <= 256; d*operand_bytes <= 768 (d <= 384 for F16_EXACT, 192 for
+ * TF32, 64 for TF32X3), ma, mb < 2^31. */
+sg_status scalegann_knn_workspace(uint64_t ma, uint64_t mb, uint32_t d, sg_dtype dtype, uint32_t L,
+                                  int32_t precision, size_t* bytes);
+sg_status scalegann_knn(const void* xa, const uint32_t* ida, uint64_t ma, const void* xb,
+                        const uint32_t* idb, uint64_t mb, sg_dtype dtype, uint32_t d, int self_exclude,
+                        uint32_t L, int32_t metric, int32_t precision, uint32_t* ids, float* dists,
+                        void* ws, size_t ws_bytes, void* stream);
+
+/* ---- a6: rank-based detour-count prune (reading R10) ------------------------
+ * knn m x L (local ids, rows sorted by (dist,id)) -> out m x R: the first R
+ * ranks in the stable order by (detour count, rank), sentinel ranks last;
+ * out_d carries the kNN distances.  Bit-exact with the oracle. L <= 256. */
+sg_status scalegann_prune(const uint32_t* knn_ids, const float* knn_d, uint64_t m, uint32_t L,
+                          uint32_t R, uint32_t rule, uint32_t* out, float* out_d, void* stream);
+
+/* ---- a7: reverse-edge insertion (reading R11) -------------------------------
+ * pruned m x R -> out m x R = pruned[y][0..h) ++ first R-h of
+ * (rev_np ++ remaining forward), rev ordered by (rank, source) and capped at R.
+ * Bit-exact with the oracle.  R <= 128. */
+sg_status scalegann_reverse_workspace(uint64_t m, uint32_t R, size_t* bytes);
+sg_status scalegann_reverse(const uint32_t* pruned, const float* pruned_d, uint64_t m, uint32_t R,
+                            uint32_t h, uint32_t* out, float* out_d, void* ws, size_t ws_bytes,
+                            void* stream);
+
+/* ---- a4-a7: one shard build ("invokes a GPU-based indexing algorithm") --
+ * gather rows idmap[0..m) of x, exact kNN (a5), prune (a6), reverse (a7).
+ * knn_ids/knn_d (m x L) may be NULL (then kept in ws).  graph/graph_d m x R
+ * local ids.  Errors: SG_ERR_TOO_SMALL when m < 2. */
+sg_status scalegann_build_shard_workspace(uint64_t m, uint32_t d, sg_dtype dtype,
+                                          const sg_build_params* p, size_t* bytes);
+sg_status scalegann_build_shard(const void* x, sg_dtype dtype, uint64_t n, uint32_t d,
+                                const uint32_t* idmap, uint64_t m, const sg_build_params* p,
+                                uint32_t* knn_ids, float* knn_d, uint32_t* graph, float* graph_d,
+                                void* ws, size_t ws_bytes, void* stream);
+/* prune + reverse only: the parity entry point fed with an external kNN */
+sg_status scalegann_optimize_from_knn(const uint32_t* knn_ids, const float* knn_d, uint64_t m,
+                                      const sg_build_params* p, uint32_t* graph, float* graph_d,
+                                      void* ws, size_t ws_bytes, void* stream);
+
+/* ---- a8: cross-shard merge by edge union + re-prune (R12) ----
+ * Distributed protocol (one rank per GPU; shard s built on rank owner[s]):
+ *   1. scalegann_merge_counts: per destination rank, how many replica rows
+ *      this rank sends and receives (both computable locally from home[]).
+ *   2. scalegann_merge_pack: record per (g, h>=1) with shard home[g][h] owned
+ *      here, sent to owner[home[g][0]]: words [g, h, R global ids, R dist bits];
+ *      records grouped by destination, ascending (g, h) within one.
+ *   3. the caller exchanges the records (NCCL all-to-all over NVLink).
+ *   4. scalegann_merge_union: for each g whose primary shard is owned here,
+ *      union of the primary row and the received rows, dedupe by gid keeping
+ *      the minimum distance, sort by (dist, gid), first R -> merged[g] (rows of
+ *      n x R, only those owned here are written).
+ * idmaps/graphs/graphs_d: HOST arrays of k DEVICE pointers (NULL for shards
+ * not built here).  inv: n x omega local ids (scalegann_shard_idmap).  owner_host: k ranks.
+ * Record size in uint32 words = 2 + 2R. */
+sg_status scalegann_merge_counts(const uint32_t* home, uint64_t n, uint32_t omega, uint32_t k,
+                                 const int32_t* owner_host, int rank, int world,
+                                 uint64_t* send_host, uint64_t* recv_host, void* ws, size_t ws_bytes,
+                                 void* stream);
+sg_status scalegann_merge_workspace(uint64_t n, uint32_t omega, uint32_t k, int world, size_t* bytes);
+sg_status scalegann_merge_pack(const uint32_t* home, const uint32_t* inv, uint64_t n, uint32_t omega,
+                               uint32_t k, const int32_t* owner_host, int rank, int world,
+                               const uint32_t* const* idmaps, const uint32_t* const* graphs,
+                               const float* const* graphs_d, uint32_t R, uint32_t* sendbuf,
+                               void* ws, size_t ws_bytes, void* stream);
+sg_status scalegann_merge_union(const uint32_t* home, const uint32_t* inv, uint64_t n, uint32_t omega,
+                                uint32_t k, const int32_t* owner_host, int rank,
+                                const uint32_t* const* idmaps, const uint32_t* const* graphs,
+                                const float* const* graphs_d, uint32_t R, const uint32_t* recvbuf,
+                                uint64_t n_recv, uint32_t* merged, float* merged_d, void* ws,
+                                size_t ws_bytes, void* stream);
+/* single-process merge of all k shards (owner = 0 for every shard) */
+sg_status scalegann_merge(const uint32_t* home, const uint32_t* inv, uint64_t n, uint32_t omega,
+                          uint32_t k, const uint32_t* const* idmaps, const uint32_t* const* graphs,
+                          const float* const* graphs_d, uint32_t R, uint32_t* merged, float* merged_d,
+                          void* ws, size_t ws_bytes, void* stream);
+
+/* ---- a9: recall evaluation (reading R14) ------------------
+ * Greedy best-first beam search from `entry` over graph (n x R global ids) for
+ * nq queries (nq x d, same dtype as x); out_ids nq x topk.  gt (nq x topk,
+ * device) may be NULL, then it is computed exactly with scalegann_knn and
+ * written to gt_out (if not NULL).  recall_host = |ret & gt| / (nq*topk);
+ * synchronises.  beam <= 512, topk <= beam, R <= 128. */
+sg_status scalegann_search_workspace(uint64_t n, uint32_t d, sg_dtype dtype, uint32_t nq, uint32_t topk,
+                                     uint32_t beam, size_t* bytes);
+sg_status scalegann_search_eval(const void* x, sg_dtype dtype, uint64_t n, uint32_t d,
+                                const uint32_t* graph, uint32_t R, uint32_t entry, const void* queries,
+                                uint32_t nq, uint32_t topk, uint32_t beam, int32_t metric,
+                                const uint32_t* gt, uint32_t* gt_out, uint32_t* out_ids,
+                                double* recall_host, void* ws, size_t ws_bytes, void* stream);
+
+/* ---- diagnostics ------------------------------------------------------------
+ * Raw distance-tile probe of the tcgen05 GEMM core (validation of the MMA
+ * pipeline against a reference matmul): out[i][j] = a_i . b_j in fp32 for
+ * 0 <= i < ma, 0 <= j < mb (operands converted as for `precision`). */
+sg_status scalegann_gemm_probe(const void* xa, uint64_t ma, const void* xb, uint64_t mb, sg_dtype dtype,
+                               uint32_t d, int32_t precision, float* out, void* ws, size_t ws_bytes,
+                               void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SCALEGANN_H */

@@ -1,0 +1,411 @@
+"""Thin Python binding of libscalegann.so (include/scalegann.h), same names as the C ABI.
+
+Argument marshalling only: every step of the path runs in the library's CUDA kernels.
+torch supplies device memory (tensors, workspaces) and the current CUDA stream.  There is no
+CPU fallback: if the extension is missing or a call fails, a ScaleGannError is raised.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+from . import build as _build
+
+SENT = 0xFFFFFFFF
+SG_U8, SG_F32 = 0, 1
+SG_L2, SG_IP = 0, 1
+PREC_AUTO, PREC_F16_EXACT, PREC_TF32, PREC_TF32X3 = 0, 1, 2, 3
+_STATUS = {0: "SG_OK", 1: "SG_ERR_INVALID_ARG", 2: "SG_ERR_UNSUPPORTED", 3: "SG_ERR_CUDA",
+           4: "SG_ERR_CAPACITY", 5: "SG_ERR_WORKSPACE", 6: "SG_ERR_TOO_SMALL"}
+
+
+class ScaleGannError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class PartitionParams(ctypes.Structure):
+    _fields_ = [("k", ctypes.c_uint32), ("omega", ctypes.c_uint32), ("epsilon", ctypes.c_float),
+                ("theta0_ppm", ctypes.c_uint32), ("alpha", ctypes.c_float), ("block_size", ctypes.c_uint32),
+                ("capacity", ctypes.c_uint64)]
+
+
+class BuildParams(ctypes.Structure):
+    _fields_ = [("L", ctypes.c_uint32), ("R", ctypes.c_uint32), ("metric", ctypes.c_int32),
+                ("precision", ctypes.c_int32), ("prune_rule", ctypes.c_uint32),
+                ("protected_edges", ctypes.c_uint32)]
+
+
+_lib = None
+EXPORTS = [
+    "scalegann_abi_version", "scalegann_last_error", "scalegann_kmeans_workspace", "scalegann_kmeans",
+    "scalegann_partition_workspace", "scalegann_partition", "scalegann_shard_idmap_workspace",
+    "scalegann_shard_idmap", "scalegann_entry_points", "scalegann_knn_workspace", "scalegann_knn",
+    "scalegann_prune", "scalegann_reverse_workspace", "scalegann_reverse", "scalegann_build_shard_workspace",
+    "scalegann_build_shard", "scalegann_optimize_from_knn", "scalegann_merge_counts", "scalegann_merge_workspace",
+    "scalegann_merge_pack", "scalegann_merge_union", "scalegann_merge", "scalegann_search_workspace",
+    "scalegann_search_eval", "scalegann_gemm_probe",
+]
+
+
+def lib_path() -> str:
+    return _build.LIB
+
+
+def load(build_if_missing: bool = True):
+    """Load libscalegann.so (building it with nvcc if it is missing or stale)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if build_if_missing:
+        _build.build()
+    if not os.path.exists(_build.LIB):
+        raise ImportError(f"libscalegann.so not found at {_build.LIB}; run paper_2605_10135_b200.build")
+    L = ctypes.CDLL(_build.LIB)
+    vp, u64, u32, i32, f32, sz = (ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int32,
+                                  ctypes.c_float, ctypes.c_size_t)
+    psz = ctypes.POINTER(ctypes.c_size_t)
+    pu64 = ctypes.POINTER(ctypes.c_uint64)
+    pu32 = ctypes.POINTER(ctypes.c_uint32)
+    P = ctypes.POINTER
+    sig = {
+        "scalegann_abi_version": ([], ctypes.c_int),
+        "scalegann_last_error": ([], ctypes.c_char_p),
+        "scalegann_kmeans_workspace": ([u64, u32, u32, u32, psz], i32),
+        "scalegann_kmeans": ([vp, i32, u64, u32, u32, u64, u32, u32, vp, vp, sz, vp], i32),
+        "scalegann_partition_workspace": ([u64, u32, P(PartitionParams), psz], i32),
+        "scalegann_partition": ([vp, i32, u64, u32, vp, P(PartitionParams), vp, vp, pu64, vp, sz, vp], i32),
+        "scalegann_shard_idmap_workspace": ([u64, psz], i32),
+        "scalegann_shard_idmap": ([vp, u64, u32, u32, vp, vp, pu64, vp, sz, vp], i32),
+        "scalegann_entry_points": ([vp, vp, u64, u32, u32, pu64, pu32, pu32, vp, sz, vp], i32),
+        "scalegann_knn_workspace": ([u64, u64, u32, i32, u32, i32, psz], i32),
+        "scalegann_knn": ([vp, vp, u64, vp, vp, u64, i32, u32, ctypes.c_int, u32, i32, i32, vp, vp, vp, sz, vp], i32),
+        "scalegann_prune": ([vp, vp, u64, u32, u32, u32, vp, vp, vp], i32),
+        "scalegann_reverse_workspace": ([u64, u32, psz], i32),
+        "scalegann_reverse": ([vp, vp, u64, u32, u32, vp, vp, vp, sz, vp], i32),
+        "scalegann_build_shard_workspace": ([u64, u32, i32, P(BuildParams), psz], i32),
+        "scalegann_build_shard": ([vp, i32, u64, u32, vp, u64, P(BuildParams), vp, vp, vp, vp, vp, sz, vp], i32),
+        "scalegann_optimize_from_knn": ([vp, vp, u64, P(BuildParams), vp, vp, vp, sz, vp], i32),
+        "scalegann_merge_counts": ([vp, u64, u32, u32, P(i32), ctypes.c_int, ctypes.c_int, pu64, pu64, vp, sz, vp],
+                                   i32),
+        "scalegann_merge_workspace": ([u64, u32, u32, ctypes.c_int, psz], i32),
+        "scalegann_merge_pack": ([vp, vp, u64, u32, u32, P(i32), ctypes.c_int, ctypes.c_int, P(vp), P(vp), P(vp), u32,
+                                  vp, vp, sz, vp], i32),
+        "scalegann_merge_union": ([vp, vp, u64, u32, u32, P(i32), ctypes.c_int, P(vp), P(vp), P(vp), u32, vp, u64, vp,
+                                   vp, vp, sz, vp], i32),
+        "scalegann_merge": ([vp, vp, u64, u32, u32, P(vp), P(vp), P(vp), u32, vp, vp, vp, sz, vp], i32),
+        "scalegann_search_workspace": ([u64, u32, i32, u32, u32, u32, psz], i32),
+        "scalegann_search_eval": ([vp, i32, u64, u32, vp, u32, u32, vp, u32, u32, u32, i32, vp, vp, vp,
+                                   P(ctypes.c_double), vp, sz, vp], i32),
+        "scalegann_gemm_probe": ([vp, u64, vp, u64, i32, u32, i32, vp, vp, sz, vp], i32),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = L
+    return L
+
+
+def _check(st: int):
+    if st != 0:
+        msg = _lib.scalegann_last_error().decode(errors="replace")
+        raise ScaleGannError(st, msg)
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _dtype(x: torch.Tensor) -> int:
+    if x.dtype == torch.uint8:
+        return SG_U8
+    if x.dtype == torch.float32:
+        return SG_F32
+    raise TypeError(f"vectors must be uint8 or float32, got {x.dtype}")
+
+
+def _dev(t: torch.Tensor, name: str):
+    if not t.is_cuda or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous CUDA tensor")
+
+
+class Workspace:
+    """A reusable device scratch buffer (grows on demand)."""
+
+    def __init__(self, device=None):
+        self.buf = None
+        self.device = device
+
+    def get(self, nbytes: int) -> torch.Tensor:
+        nbytes = max(int(nbytes), 256)
+        if self.buf is None or self.buf.numel() < nbytes:
+            self.buf = torch.empty(nbytes, dtype=torch.uint8, device=self.device or "cuda")
+        return self.buf
+
+
+_WS = {}
+
+
+def _ws(nbytes: int, ws: Workspace | None):
+    if ws is None:
+        dev = torch.cuda.current_device()
+        ws = _WS.setdefault(dev, Workspace(f"cuda:{dev}"))
+    buf = ws.get(nbytes)
+    return _ptr(buf), buf.numel()
+
+
+def _size_q(fn, *args) -> int:
+    out = ctypes.c_size_t(0)
+    _check(fn(*args, ctypes.byref(out)))
+    return out.value
+
+
+# ----------------------------------------------------------------------------- a1
+def scalegann_kmeans(x, k, seed=42, max_iter=15, spc=256, ws=None):
+    L = load()
+    _dev(x, "x")
+    n, d = x.shape
+    C = torch.empty(k, d, dtype=torch.float32, device=x.device)
+    nb = _size_q(L.scalegann_kmeans_workspace, n, d, k, spc)
+    p, nbytes = _ws(nb, ws)
+    _check(L.scalegann_kmeans(_ptr(x), _dtype(x), n, d, k, seed, max_iter, spc, _ptr(C), p, nbytes, _stream()))
+    return C
+
+
+# ----------------------------------------------------------------------------- a2-a3
+def scalegann_partition(x, centroids, omega=2, epsilon=1.2, theta0_ppm=400_000, alpha=1.0, block_size=65536,
+                        capacity=0, ws=None):
+    """Returns (home n x omega uint32, primary_d n float32, counts dict of numpy-free python lists)."""
+    L = load()
+    _dev(x, "x")
+    _dev(centroids, "centroids")
+    n, d = x.shape
+    k = centroids.shape[0]
+    prm = PartitionParams(k, omega, epsilon, theta0_ppm, alpha, block_size, capacity)
+    home = torch.empty(n, omega, dtype=torch.int32, device=x.device)
+    pd = torch.empty(n, dtype=torch.float32, device=x.device)
+    counts = (ctypes.c_uint64 * (3 * k))()
+    nb = _size_q(L.scalegann_partition_workspace, n, d, ctypes.byref(prm))
+    p, nbytes = _ws(nb, ws)
+    _check(L.scalegann_partition(_ptr(x), _dtype(x), n, d, _ptr(centroids), ctypes.byref(prm), _ptr(home), _ptr(pd),
+                                 counts, p, nbytes, _stream()))
+    c = list(counts)
+    return home, pd, {"sizes": c[:k], "prim": c[k:2 * k], "repl": c[2 * k:]}
+
+
+# ----------------------------------------------------------------------------- a4
+def scalegann_shard_idmap(home, shard, m=None, inv=None, ws=None):
+    """idmap (int32 view of uint32 ids) of `shard`; fills inv (n x omega) if given."""
+    L = load()
+    _dev(home, "home")
+    n, omega = home.shape
+    nb = _size_q(L.scalegann_shard_idmap_workspace, n)
+    p, nbytes = _ws(nb, ws)
+    if m is None:
+        mh = ctypes.c_uint64(0)
+        _check(L.scalegann_shard_idmap(_ptr(home), n, omega, shard, None, None, ctypes.byref(mh), p, nbytes, _stream()))
+        m = mh.value
+    idmap = torch.empty(max(m, 1), dtype=torch.int32, device=home.device)
+    _check(L.scalegann_shard_idmap(_ptr(home), n, omega, shard, _ptr(idmap), _ptr(inv), None, p, nbytes, _stream()))
+    return idmap[:m]
+
+
+def scalegann_entry_points(home, primary_d, sizes, ws=None):
+    L = load()
+    n, omega = home.shape
+    k = len(sizes)
+    sz = (ctypes.c_uint64 * k)(*sizes)
+    ent = (ctypes.c_uint32 * k)()
+    g = ctypes.c_uint32(0)
+    p, nbytes = _ws(64 * 8 + 1024, ws)
+    _check(L.scalegann_entry_points(_ptr(home), _ptr(primary_d), n, omega, k, sz, ent, ctypes.byref(g), p, nbytes,
+                                    _stream()))
+    return g.value, list(ent)
+
+
+# ----------------------------------------------------------------------------- a5
+def scalegann_knn(xa, L_, xb=None, ida=None, idb=None, self_exclude=True, metric=SG_L2, precision=PREC_AUTO,
+                  ws=None):
+    """Exact top-L: returns (ids ma x L int32 [uint32 bits], dists ma x L float32)."""
+    L = load()
+    _dev(xa, "xa")
+    same = xb is None
+    if same:
+        xb, idb = xa, ida
+    _dev(xb, "xb")
+    d = xa.shape[1]
+    ma = xa.shape[0] if ida is None else ida.numel()
+    mb = xb.shape[0] if idb is None else idb.numel()
+    ids = torch.empty(ma, L_, dtype=torch.int32, device=xa.device)
+    dist = torch.empty(ma, L_, dtype=torch.float32, device=xa.device)
+    nb = _size_q(L.scalegann_knn_workspace, ma, mb, d, _dtype(xa), L_, precision)
+    p, nbytes = _ws(nb, ws)
+    _check(L.scalegann_knn(_ptr(xa), _ptr(ida), ma, _ptr(xb), _ptr(idb), mb, _dtype(xa), d, int(self_exclude), L_,
+                           metric, precision, _ptr(ids), _ptr(dist), p, nbytes, _stream()))
+    return ids, dist
+
+
+def scalegann_gemm_probe(xa, xb, precision=PREC_AUTO, ws=None):
+    L = load()
+    ma, d = xa.shape
+    mb = xb.shape[0]
+    out = torch.zeros(ma, mb, dtype=torch.float32, device=xa.device)
+    nb = _size_q(L.scalegann_knn_workspace, ma, mb, d, _dtype(xa), 1, precision)
+    p, nbytes = _ws(nb, ws)
+    _check(L.scalegann_gemm_probe(_ptr(xa), ma, _ptr(xb), mb, _dtype(xa), d, precision, _ptr(out), p, nbytes,
+                                  _stream()))
+    return out
+
+
+# ----------------------------------------------------------------------------- a6 / a7
+def scalegann_prune(knn_ids, knn_d, R, rule=0):
+    L = load()
+    m, L_ = knn_ids.shape
+    out = torch.empty(m, R, dtype=torch.int32, device=knn_ids.device)
+    od = torch.empty(m, R, dtype=torch.float32, device=knn_ids.device)
+    _check(L.scalegann_prune(_ptr(knn_ids), _ptr(knn_d), m, L_, R, rule, _ptr(out), _ptr(od), _stream()))
+    return out, od
+
+
+def scalegann_reverse(pruned, pruned_d, protected=None, ws=None):
+    L = load()
+    m, R = pruned.shape
+    h = R // 2 if protected is None else protected
+    out = torch.empty(m, R, dtype=torch.int32, device=pruned.device)
+    od = torch.empty(m, R, dtype=torch.float32, device=pruned.device)
+    nb = _size_q(L.scalegann_reverse_workspace, m, R)
+    p, nbytes = _ws(nb, ws)
+    _check(L.scalegann_reverse(_ptr(pruned), _ptr(pruned_d), m, R, h, _ptr(out), _ptr(od), p, nbytes, _stream()))
+    return out, od
+
+
+def build_params(L_, R, metric=SG_L2, precision=PREC_AUTO, prune_rule=0, protected_edges=0):
+    return BuildParams(L_, R, metric, precision, prune_rule, protected_edges)
+
+
+def scalegann_build_shard(x, idmap, L_, R, metric=SG_L2, precision=PREC_AUTO, prune_rule=0, protected_edges=0,
+                          keep_knn=False, ws=None):
+    """gather + exact kNN + prune + reverse for one shard; returns (graph, graph_d[, knn_ids, knn_d])."""
+    L = load()
+    _dev(x, "x")
+    n, d = x.shape
+    m = idmap.numel()
+    prm = build_params(L_, R, metric, precision, prune_rule, protected_edges)
+    g = torch.empty(m, R, dtype=torch.int32, device=x.device)
+    gd = torch.empty(m, R, dtype=torch.float32, device=x.device)
+    kid = torch.empty(m, L_, dtype=torch.int32, device=x.device) if keep_knn else None
+    kd = torch.empty(m, L_, dtype=torch.float32, device=x.device) if keep_knn else None
+    nb = _size_q(L.scalegann_build_shard_workspace, m, d, _dtype(x), ctypes.byref(prm))
+    p, nbytes = _ws(nb, ws)
+    _check(L.scalegann_build_shard(_ptr(x), _dtype(x), n, d, _ptr(idmap), m, ctypes.byref(prm), _ptr(kid), _ptr(kd),
+                                   _ptr(g), _ptr(gd), p, nbytes, _stream()))
+    return (g, gd, kid, kd) if keep_knn else (g, gd)
+
+
+def scalegann_optimize_from_knn(knn_ids, knn_d, R, prune_rule=0, protected_edges=0, ws=None):
+    L = load()
+    m, L_ = knn_ids.shape
+    prm = build_params(L_, R, SG_L2, PREC_AUTO, prune_rule, protected_edges)
+    g = torch.empty(m, R, dtype=torch.int32, device=knn_ids.device)
+    gd = torch.empty(m, R, dtype=torch.float32, device=knn_ids.device)
+    nb = _size_q(L.scalegann_build_shard_workspace, m, 1, SG_F32, ctypes.byref(prm))
+    p, nbytes = _ws(nb, ws)
+    _check(L.scalegann_optimize_from_knn(_ptr(knn_ids), _ptr(knn_d), m, ctypes.byref(prm), _ptr(g), _ptr(gd), p,
+                                         nbytes, _stream()))
+    return g, gd
+
+
+# ----------------------------------------------------------------------------- a8
+def _ptr_array(ts, k):
+    arr = (ctypes.c_void_p * k)()
+    for s in range(k):
+        arr[s] = ts[s].data_ptr() if ts[s] is not None else None
+    return arr
+
+
+def scalegann_merge_counts(home, k, owner, rank, world, ws=None):
+    L = load()
+    n, omega = home.shape
+    own = (ctypes.c_int32 * k)(*owner)
+    send = (ctypes.c_uint64 * world)()
+    recv = (ctypes.c_uint64 * world)()
+    nb = _size_q(L.scalegann_merge_workspace, n, omega, k, world)
+    p, nbytes = _ws(nb, ws)
+    _check(L.scalegann_merge_counts(_ptr(home), n, omega, k, own, rank, world, send, recv, p, nbytes, _stream()))
+    return list(send), list(recv)
+
+
+def scalegann_merge_pack(home, inv, owner, rank, world, idmaps, graphs, graphs_d, n_send, ws=None):
+    L = load()
+    n, omega = home.shape
+    k = len(owner)
+    R = next(g for g in graphs if g is not None).shape[1]
+    W = 2 + 2 * R
+    sendbuf = torch.empty(max(n_send, 1) * W, dtype=torch.int32, device=home.device)
+    nb = _size_q(L.scalegann_merge_workspace, n, omega, k, world)
+    p, nbytes = _ws(nb, ws)
+    _check(L.scalegann_merge_pack(_ptr(home), _ptr(inv), n, omega, k, (ctypes.c_int32 * k)(*owner), rank, world,
+                                  _ptr_array(idmaps, k), _ptr_array(graphs, k), _ptr_array(graphs_d, k), R,
+                                  _ptr(sendbuf), p, nbytes, _stream()))
+    return sendbuf[: n_send * W]
+
+
+def scalegann_merge_union(home, inv, owner, rank, idmaps, graphs, graphs_d, recvbuf, n_recv, merged=None,
+                          merged_d=None, ws=None):
+    L = load()
+    n, omega = home.shape
+    k = len(owner)
+    R = next(g for g in graphs if g is not None).shape[1]
+    if merged is None:
+        merged = torch.full((n, R), -1, dtype=torch.int32, device=home.device)
+        merged_d = torch.full((n, R), float("inf"), dtype=torch.float32, device=home.device)
+    nb = _size_q(L.scalegann_merge_workspace, n, omega, k, 1)
+    p, nbytes = _ws(nb, ws)
+    _check(L.scalegann_merge_union(_ptr(home), _ptr(inv), n, omega, k, (ctypes.c_int32 * k)(*owner), rank,
+                                   _ptr_array(idmaps, k), _ptr_array(graphs, k), _ptr_array(graphs_d, k), R,
+                                   _ptr(recvbuf), n_recv, _ptr(merged), _ptr(merged_d), p, nbytes, _stream()))
+    return merged, merged_d
+
+
+def scalegann_merge(home, inv, idmaps, graphs, graphs_d, ws=None):
+    """Single-process merge of all k shards."""
+    L = load()
+    n, omega = home.shape
+    k = len(idmaps)
+    R = graphs[0].shape[1]
+    merged = torch.empty(n, R, dtype=torch.int32, device=home.device)
+    merged_d = torch.empty(n, R, dtype=torch.float32, device=home.device)
+    nrec = int((home[:, 1:] != -1).sum().item()) if omega > 1 else 0
+    nb = _size_q(L.scalegann_merge_workspace, n, omega, k, 1) + nrec * (2 + 2 * R) * 4 + 4096
+    p, nbytes = _ws(nb, ws)
+    _check(L.scalegann_merge(_ptr(home), _ptr(inv), n, omega, k, _ptr_array(idmaps, k), _ptr_array(graphs, k),
+                             _ptr_array(graphs_d, k), R, _ptr(merged), _ptr(merged_d), p, nbytes, _stream()))
+    return merged, merged_d
+
+
+# ----------------------------------------------------------------------------- a9
+def scalegann_search_eval(x, graph, entry, queries, topk=10, beam=64, metric=SG_L2, gt=None, ws=None):
+    """Returns (out_ids nq x topk, gt nq x topk, recall)."""
+    L = load()
+    n, d = x.shape
+    R = graph.shape[1]
+    nq = queries.shape[0]
+    out = torch.empty(nq, topk, dtype=torch.int32, device=x.device)
+    gt_out = None
+    if gt is None:
+        gt_out = torch.empty(nq, topk, dtype=torch.int32, device=x.device)
+    rec = ctypes.c_double(0.0)
+    nb = _size_q(L.scalegann_search_workspace, n, d, _dtype(x), nq, topk, beam)
+    p, nbytes = _ws(nb, ws)
+    _check(L.scalegann_search_eval(_ptr(x), _dtype(x), n, d, _ptr(graph), R, entry, _ptr(queries), nq, topk, beam,
+                                   metric, _ptr(gt), _ptr(gt_out), _ptr(out), ctypes.byref(rec), p, nbytes,
+                                   _stream()))
+    return out, (gt if gt is not None else gt_out), rec.value

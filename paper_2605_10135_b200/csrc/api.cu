@@ -1,0 +1,373 @@
+// extern "C" entry points of libscalegann.so (include/scalegann.h): argument validation,
+// workspace carving and dispatch to the stage kernels.  No torch, no host fallback: every
+// step of the path runs in this library's kernels.
+#include <stdarg.h>
+
+#include "common.cuh"
+
+namespace sg {
+// stage entry points implemented in the per-stage translation units
+size_t kmeans_ws(uint64_t n, uint32_t d, uint32_t k, uint32_t spc);
+sg_status kmeans_run(const void* x, sg_dtype dtype, uint64_t n, uint32_t d, uint32_t k, uint64_t seed,
+                     uint32_t max_iter, uint32_t spc, float* C, void* ws, size_t ws_bytes, cudaStream_t st);
+size_t partition_ws(uint64_t n, uint32_t k);
+sg_status partition_run(const void* x, sg_dtype dtype, uint64_t n, uint32_t d, const float* C,
+                        const sg_partition_params* p, uint32_t* home, float* primary_d, uint64_t* counts_host,
+                        void* ws, size_t ws_bytes, cudaStream_t st);
+size_t idmap_ws(uint64_t n);
+sg_status idmap_run(const uint32_t* home, uint64_t n, uint32_t omega, uint32_t s, uint32_t* idmap, uint32_t* inv,
+                    uint64_t* m_host, void* ws, size_t ws_bytes, cudaStream_t st);
+sg_status entry_run(const uint32_t* home, const float* pd, uint64_t n, uint32_t omega, uint32_t k,
+                    const uint64_t* sizes_host, uint32_t* entry_host, uint32_t* global_host, void* ws,
+                    size_t ws_bytes, cudaStream_t st);
+size_t reverse_ws(uint64_t m, uint32_t R);
+sg_status merge_counts_run(const uint32_t* home, uint64_t n, uint32_t omega, uint32_t k, const int32_t* owner,
+                           int rank, int world, uint64_t* send_host, uint64_t* recv_host, void* ws, size_t ws_bytes,
+                           cudaStream_t st);
+size_t merge_ws(uint64_t n, uint32_t omega);
+sg_status merge_pack_run(const uint32_t* home, const uint32_t* inv, uint64_t n, uint32_t omega, uint32_t k,
+                         const int32_t* owner, int rank, int world, const uint32_t* const* idmaps,
+                         const uint32_t* const* graphs, const float* const* graphs_d, uint32_t R, uint32_t* sendbuf,
+                         void* ws, size_t ws_bytes, cudaStream_t st);
+sg_status merge_union_run(const uint32_t* home, const uint32_t* inv, uint64_t n, uint32_t omega, uint32_t k,
+                          const int32_t* owner, int rank, const uint32_t* const* idmaps, const uint32_t* const* graphs,
+                          const float* const* graphs_d, uint32_t R, const uint32_t* recvbuf, uint64_t n_recv,
+                          uint32_t* merged, float* merged_d, void* ws, size_t ws_bytes, cudaStream_t st);
+size_t beam_ws(uint64_t n, uint32_t nq);
+sg_status beam_run(const void* x, sg_dtype dtype, uint64_t n, uint32_t d, const uint32_t* graph, uint32_t R,
+                   uint32_t entry, const void* q, uint32_t nq, uint32_t topk, uint32_t beam, int metric,
+                   uint32_t* out_ids, unsigned long long* ndist, Carver& cv, cudaStream_t st);
+sg_status recall_run(const uint32_t* ret, const uint32_t* gt, uint32_t nq, uint32_t topk, double* recall_host,
+                     Carver& cv, cudaStream_t st);
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+sg_status cuda_status(cudaError_t e, const char* what) {
+    set_error("CUDA error %s (%d) in %s", cudaGetErrorString(e), (int)e, what);
+    return SG_ERR_CUDA;
+}
+
+static uint32_t knn_kdim_bytes(int prec, uint32_t d) {
+    return operand_kdim(prec, d) * (prec == SG_PREC_F16_EXACT ? 2u : 4u);
+}
+
+// workspace of a kNN between ma rows and mb rows (both gathered); `same` = self-join
+static size_t knn_total_ws(uint64_t ma, uint64_t mb, uint32_t d, int prec, uint32_t L, bool same) {
+    size_t b = operand_bytes(prec, d, ma) + (same ? 0 : operand_bytes(prec, d, mb));
+    return b + knn_core_workspace(L) + 4096;
+}
+
+static int worst_prec(sg_dtype dtype, int32_t precision) {
+    // AUTO resolves at run time; size the workspace for the widest candidate
+    if (precision != SG_PREC_AUTO) return precision;
+    return dtype == SG_U8 ? SG_PREC_TF32 : SG_PREC_TF32;
+}
+
+static sg_status check_knn_shape(int prec, uint32_t d, uint32_t L) {
+    SG_CHECK_ARG(L >= 1 && L <= 256, "kNN: L must be in [1, 256]");
+    const uint32_t kb = knn_kdim_bytes(prec, d);
+    if (kb > 768) {
+        set_error("kNN: d=%u needs %u operand bytes per row with this precision (max 768)", d, kb);
+        return SG_ERR_UNSUPPORTED;
+    }
+    return SG_OK;
+}
+
+}  // namespace sg
+
+using namespace sg;
+
+extern "C" {
+
+int scalegann_abi_version(void) { return SCALEGANN_ABI_VERSION; }
+const char* scalegann_last_error(void) { return g_err; }
+
+// ------------------------------------------------------------------ a1
+sg_status scalegann_kmeans_workspace(uint64_t n, uint32_t d, uint32_t k, uint32_t spc, size_t* bytes) {
+    SG_CHECK_ARG(bytes, "null bytes");
+    *bytes = kmeans_ws(n, d, k, spc);
+    return SG_OK;
+}
+sg_status scalegann_kmeans(const void* x, sg_dtype dtype, uint64_t n, uint32_t d, uint32_t k, uint64_t seed,
+                           uint32_t max_iter, uint32_t spc, float* centroids, void* ws, size_t ws_bytes, void* stream) {
+    SG_CHECK_ARG(x && centroids && n > 0 && d > 0 && d <= 1024 && k >= 1 && k <= 64 && spc >= 1,
+                 "kmeans: bad arguments (n>0, 0<d<=1024, 1<=k<=64)");
+    SG_CHECK_ARG(dtype == SG_U8 || dtype == SG_F32, "kmeans: bad dtype");
+    return kmeans_run(x, dtype, n, d, k, seed, max_iter, spc, centroids, ws, ws_bytes, S(stream));
+}
+
+// ------------------------------------------------------------------ a2-a3
+sg_status scalegann_partition_workspace(uint64_t n, uint32_t d, const sg_partition_params* p, size_t* bytes) {
+    SG_CHECK_ARG(p && bytes, "null argument");
+    (void)d;
+    *bytes = partition_ws(n, p->k);
+    return SG_OK;
+}
+sg_status scalegann_partition(const void* x, sg_dtype dtype, uint64_t n, uint32_t d, const float* centroids,
+                              const sg_partition_params* p, uint32_t* home, float* primary_d, uint64_t* counts_host,
+                              void* ws, size_t ws_bytes, void* stream) {
+    SG_CHECK_ARG(x && centroids && p && home && primary_d, "partition: null pointer");
+    SG_CHECK_ARG(n > 0 && n < 0xFFFFFFFFull && d > 0, "partition: need 0 < n < 2^32-1, d > 0");
+    SG_CHECK_ARG(dtype == SG_U8 || dtype == SG_F32, "partition: bad dtype");
+    SG_CHECK_ARG(p->k >= 1 && p->k <= 64, "partition: k must be in [1, 64]");
+    SG_CHECK_ARG(p->omega >= 1 && p->omega <= p->k, "partition: omega must be in [1, k]");
+    SG_CHECK_ARG(p->epsilon > 0.f, "partition: epsilon must be > 0");
+    SG_CHECK_ARG(p->theta0_ppm > 0 && p->theta0_ppm < 1000000, "partition: theta0_ppm must be in (0, 1e6)");
+    SG_CHECK_ARG(p->block_size >= 1 && p->block_size <= (1u << 24), "partition: block_size in [1, 2^24]");
+    return partition_run(x, dtype, n, d, centroids, p, home, primary_d, counts_host, ws, ws_bytes, S(stream));
+}
+
+// ------------------------------------------------------------------ a4
+sg_status scalegann_shard_idmap_workspace(uint64_t n, size_t* bytes) {
+    SG_CHECK_ARG(bytes, "null bytes");
+    *bytes = idmap_ws(n);
+    return SG_OK;
+}
+sg_status scalegann_shard_idmap(const uint32_t* home, uint64_t n, uint32_t omega, uint32_t shard, uint32_t* idmap,
+                                uint32_t* inv, uint64_t* m_host, void* ws, size_t ws_bytes, void* stream) {
+    SG_CHECK_ARG(home && n > 0 && omega >= 1, "idmap: bad arguments");
+    return idmap_run(home, n, omega, shard, idmap, inv, m_host, ws, ws_bytes, S(stream));
+}
+
+sg_status scalegann_entry_points(const uint32_t* home, const float* primary_d, uint64_t n, uint32_t omega, uint32_t k,
+                                 const uint64_t* sizes_host, uint32_t* entry_host, uint32_t* global_entry_host,
+                                 void* ws, size_t ws_bytes, void* stream) {
+    SG_CHECK_ARG(home && primary_d && sizes_host && entry_host && k >= 1 && k <= 64, "entry_points: bad arguments");
+    return entry_run(home, primary_d, n, omega, k, sizes_host, entry_host, global_entry_host, ws, ws_bytes, S(stream));
+}
+
+// ------------------------------------------------------------------ a5
+sg_status scalegann_knn_workspace(uint64_t ma, uint64_t mb, uint32_t d, sg_dtype dtype, uint32_t L, int32_t precision,
+                                  size_t* bytes) {
+    SG_CHECK_ARG(bytes, "null bytes");
+    *bytes = knn_total_ws(ma, mb, d, worst_prec(dtype, precision), L, false);
+    return SG_OK;
+}
+
+static sg_status knn_impl(const void* xa, const uint32_t* ida, uint64_t ma, const void* xb, const uint32_t* idb,
+                          uint64_t mb, sg_dtype dtype, uint32_t d, int self_exclude, uint32_t L, int32_t metric,
+                          int32_t precision, uint32_t* ids, float* dists, float* probe, void* ws, size_t ws_bytes,
+                          cudaStream_t st) {
+    SG_CHECK_ARG(xa && xb && (ids || probe) && (dists || probe), "kNN: null pointer");
+    SG_CHECK_ARG(ma > 0 && mb > 0 && ma < (1ull << 31) && mb < (1ull << 31) && d > 0, "kNN: bad sizes");
+    SG_CHECK_ARG(dtype == SG_U8 || dtype == SG_F32, "kNN: bad dtype");
+    SG_CHECK_ARG(metric == SG_L2 || metric == SG_IP, "kNN: bad metric");
+    SG_CHECK_ARG(precision >= SG_PREC_AUTO && precision <= SG_PREC_TF32X3, "kNN: bad precision");
+    Carver cv(ws, ws_bytes);
+    unsigned* flags = cv.take<unsigned>(2);
+    if (!cv.ok()) { set_error("kNN: workspace too small"); return SG_ERR_WORKSPACE; }
+    sg_status e;
+    const int prec = resolve_precision(precision, dtype, d, xa, ida, ma, xb, idb, mb, flags, st, &e);
+    if (e != SG_OK) return e;
+    SG_TRY(check_knn_shape(prec, d, L));
+    const bool same = xa == xb && ida == idb && ma == mb;
+    Operand A, B;
+    SG_TRY(gather_operand(xa, dtype, d, ida, ma, prec, metric, false, cv, &A, st));
+    if (same) B = A;
+    else SG_TRY(gather_operand(xb, dtype, d, idb, mb, prec, metric, true, cv, &B, st));
+    if (prec == SG_PREC_TF32X3 && !same) {
+        // A side uses [hi|hi|lo]; B side uses [hi|lo|hi]: A.a and B.b are already those layouts
+    }
+    return knn_core(A, B, metric, self_exclude != 0, L, ids, dists, probe, cv, st);
+}
+
+sg_status scalegann_knn(const void* xa, const uint32_t* ida, uint64_t ma, const void* xb, const uint32_t* idb,
+                        uint64_t mb, sg_dtype dtype, uint32_t d, int self_exclude, uint32_t L, int32_t metric,
+                        int32_t precision, uint32_t* ids, float* dists, void* ws, size_t ws_bytes, void* stream) {
+    return knn_impl(xa, ida, ma, xb, idb, mb, dtype, d, self_exclude, L, metric, precision, ids, dists, nullptr, ws,
+                    ws_bytes, S(stream));
+}
+
+sg_status scalegann_gemm_probe(const void* xa, uint64_t ma, const void* xb, uint64_t mb, sg_dtype dtype, uint32_t d,
+                               int32_t precision, float* out, void* ws, size_t ws_bytes, void* stream) {
+    SG_CHECK_ARG(out, "probe: null out");
+    return knn_impl(xa, nullptr, ma, xb, nullptr, mb, dtype, d, 0, 1, SG_L2, precision, nullptr, nullptr, out, ws,
+                    ws_bytes, S(stream));
+}
+
+// ------------------------------------------------------------------ a6 / a7
+sg_status scalegann_prune(const uint32_t* knn_ids, const float* knn_d, uint64_t m, uint32_t L, uint32_t R, uint32_t rule,
+                          uint32_t* out, float* out_d, void* stream) {
+    SG_CHECK_ARG(knn_ids && knn_d && out && out_d, "prune: null pointer");
+    SG_CHECK_ARG(L >= 1 && L <= 256 && R >= 1 && R <= L && rule <= 1, "prune: need 1 <= R <= L <= 256, rule in {0,1}");
+    return launch_prune(knn_ids, knn_d, m, L, R, rule, out, out_d, S(stream));
+}
+
+sg_status scalegann_reverse_workspace(uint64_t m, uint32_t R, size_t* bytes) {
+    SG_CHECK_ARG(bytes, "null bytes");
+    *bytes = reverse_ws(m, R);
+    return SG_OK;
+}
+sg_status scalegann_reverse(const uint32_t* pruned, const float* pruned_d, uint64_t m, uint32_t R, uint32_t h,
+                            uint32_t* out, float* out_d, void* ws, size_t ws_bytes, void* stream) {
+    SG_CHECK_ARG(pruned && pruned_d && out && out_d, "reverse: null pointer");
+    SG_CHECK_ARG(R >= 1 && R <= 128 && h <= R, "reverse: need 1 <= R <= 128, h <= R");
+    Carver cv(ws, ws_bytes);
+    return launch_reverse(pruned, pruned_d, m, R, h, out, out_d, cv, S(stream));
+}
+
+// ------------------------------------------------------------------ a4-a7
+static size_t build_ws(uint64_t m, uint32_t d, sg_dtype dtype, const sg_build_params* p) {
+    const int prec = worst_prec(dtype, p->precision);
+    size_t b = 1024;
+    b += 2 * (m * p->L * 4 + 256);     // kNN ids + dists (when not caller-provided)
+    b += 2 * (m * p->R * 4 + 256);     // pruned ids + dists
+    size_t knn = operand_bytes(prec, d, m) + knn_core_workspace(p->L) + 1024;
+    size_t rev = reverse_ws(m, p->R);
+    return b + (knn > rev ? knn : rev);
+}
+
+sg_status scalegann_build_shard_workspace(uint64_t m, uint32_t d, sg_dtype dtype, const sg_build_params* p,
+                                          size_t* bytes) {
+    SG_CHECK_ARG(p && bytes, "null argument");
+    *bytes = build_ws(m, d, dtype, p);
+    return SG_OK;
+}
+
+static sg_status check_build(const sg_build_params* p, uint64_t m) {
+    SG_CHECK_ARG(p, "build: null params");
+    SG_CHECK_ARG(p->L >= 1 && p->L <= 256 && p->R >= 1 && p->R <= p->L && p->R <= 128,
+                 "build: need 1 <= R <= L <= 256, R <= 128");
+    SG_CHECK_ARG(p->metric == SG_L2 || p->metric == SG_IP, "build: bad metric");
+    SG_CHECK_ARG(p->prune_rule <= 1 && p->protected_edges <= p->R, "build: bad prune_rule/protected_edges");
+    if (m < 2) { set_error("build: shard has m < 2 vectors (S:301)"); return SG_ERR_TOO_SMALL; }
+    SG_CHECK_ARG(m < (1ull << 31), "build: m must be < 2^31");
+    return SG_OK;
+}
+
+sg_status scalegann_optimize_from_knn(const uint32_t* knn_ids, const float* knn_d, uint64_t m, const sg_build_params* p,
+                                      uint32_t* graph, float* graph_d, void* ws, size_t ws_bytes, void* stream) {
+    SG_TRY(check_build(p, m));
+    SG_CHECK_ARG(knn_ids && knn_d && graph && graph_d, "optimize: null pointer");
+    Carver cv(ws, ws_bytes);
+    uint32_t* pr = cv.take<uint32_t>(m * p->R);
+    float* prd = cv.take<float>(m * p->R);
+    if (!cv.ok()) { set_error("optimize: workspace too small"); return SG_ERR_WORKSPACE; }
+    cudaStream_t st = S(stream);
+    SG_TRY(launch_prune(knn_ids, knn_d, m, p->L, p->R, p->prune_rule, pr, prd, st));
+    const uint32_t h = p->protected_edges ? p->protected_edges : p->R / 2;
+    return launch_reverse(pr, prd, m, p->R, h, graph, graph_d, cv, st);
+}
+
+sg_status scalegann_build_shard(const void* x, sg_dtype dtype, uint64_t n, uint32_t d, const uint32_t* idmap,
+                                uint64_t m, const sg_build_params* p, uint32_t* knn_ids, float* knn_d, uint32_t* graph,
+                                float* graph_d, void* ws, size_t ws_bytes, void* stream) {
+    SG_TRY(check_build(p, m));
+    SG_CHECK_ARG(x && idmap && graph && graph_d && n > 0 && d > 0, "build: null pointer or empty input");
+    SG_CHECK_ARG(dtype == SG_U8 || dtype == SG_F32, "build: bad dtype");
+    cudaStream_t st = S(stream);
+    Carver cv(ws, ws_bytes);
+    unsigned* flags = cv.take<unsigned>(2);
+    uint32_t* kid = knn_ids ? knn_ids : cv.take<uint32_t>(m * p->L);
+    float* kd = knn_d ? knn_d : cv.take<float>(m * p->L);
+    uint32_t* pr = cv.take<uint32_t>(m * p->R);
+    float* prd = cv.take<float>(m * p->R);
+    if (!cv.ok()) { set_error("build: workspace too small"); return SG_ERR_WORKSPACE; }
+    sg_status e;
+    const int prec = resolve_precision(p->precision, dtype, d, x, idmap, m, nullptr, nullptr, 0, flags, st, &e);
+    if (e != SG_OK) return e;
+    SG_TRY(check_knn_shape(prec, d, p->L));
+    {
+        Carver kc = cv;   // the kNN scratch is reused by the reverse stage afterwards
+        Operand A;
+        SG_TRY(gather_operand(x, dtype, d, idmap, m, prec, p->metric, false, kc, &A, st));
+        SG_TRY(knn_core(A, A, p->metric, true, p->L, kid, kd, nullptr, kc, st));
+    }
+    SG_TRY(launch_prune(kid, kd, m, p->L, p->R, p->prune_rule, pr, prd, st));
+    const uint32_t h = p->protected_edges ? p->protected_edges : p->R / 2;
+    return launch_reverse(pr, prd, m, p->R, h, graph, graph_d, cv, st);
+}
+
+// ------------------------------------------------------------------ a8
+sg_status scalegann_merge_counts(const uint32_t* home, uint64_t n, uint32_t omega, uint32_t k, const int32_t* owner_host,
+                                 int rank, int world, uint64_t* send_host, uint64_t* recv_host, void* ws,
+                                 size_t ws_bytes, void* stream) {
+    SG_CHECK_ARG(home && owner_host && omega >= 1, "merge_counts: bad arguments");
+    return merge_counts_run(home, n, omega, k, owner_host, rank, world, send_host, recv_host, ws, ws_bytes, S(stream));
+}
+sg_status scalegann_merge_workspace(uint64_t n, uint32_t omega, uint32_t k, int world, size_t* bytes) {
+    SG_CHECK_ARG(bytes, "null bytes");
+    (void)k; (void)world;
+    *bytes = merge_ws(n, omega);
+    return SG_OK;
+}
+sg_status scalegann_merge_pack(const uint32_t* home, const uint32_t* inv, uint64_t n, uint32_t omega, uint32_t k,
+                               const int32_t* owner_host, int rank, int world, const uint32_t* const* idmaps,
+                               const uint32_t* const* graphs, const float* const* graphs_d, uint32_t R,
+                               uint32_t* sendbuf, void* ws, size_t ws_bytes, void* stream) {
+    SG_CHECK_ARG(home && inv && owner_host && idmaps && graphs && graphs_d && R >= 1, "merge_pack: bad arguments");
+    return merge_pack_run(home, inv, n, omega, k, owner_host, rank, world, idmaps, graphs, graphs_d, R, sendbuf, ws,
+                          ws_bytes, S(stream));
+}
+sg_status scalegann_merge_union(const uint32_t* home, const uint32_t* inv, uint64_t n, uint32_t omega, uint32_t k,
+                                const int32_t* owner_host, int rank, const uint32_t* const* idmaps,
+                                const uint32_t* const* graphs, const float* const* graphs_d, uint32_t R,
+                                const uint32_t* recvbuf, uint64_t n_recv, uint32_t* merged, float* merged_d, void* ws,
+                                size_t ws_bytes, void* stream) {
+    SG_CHECK_ARG(home && inv && owner_host && idmaps && graphs && graphs_d && merged && merged_d && R >= 1,
+                 "merge_union: bad arguments");
+    SG_CHECK_ARG(n_recv == 0 || recvbuf, "merge_union: null recvbuf");
+    return merge_union_run(home, inv, n, omega, k, owner_host, rank, idmaps, graphs, graphs_d, R, recvbuf, n_recv,
+                           merged, merged_d, ws, ws_bytes, S(stream));
+}
+sg_status scalegann_merge(const uint32_t* home, const uint32_t* inv, uint64_t n, uint32_t omega, uint32_t k,
+                          const uint32_t* const* idmaps, const uint32_t* const* graphs, const float* const* graphs_d,
+                          uint32_t R, uint32_t* merged, float* merged_d, void* ws, size_t ws_bytes, void* stream) {
+    SG_CHECK_ARG(k >= 1 && k <= 64, "merge: k must be in [1, 64]");
+    int32_t owner[64] = {0};
+    uint64_t send = 0;
+    SG_TRY(merge_counts_run(home, n, omega, k, owner, 0, 1, &send, nullptr, ws, ws_bytes, S(stream)));
+    // the record buffer sits after the merge scratch in the same workspace
+    const size_t mw = merge_ws(n, omega);
+    const size_t need = mw + send * (2 + 2 * (size_t)R) * 4 + 256;
+    if (ws_bytes < need) { set_error("merge: workspace too small (need %zu)", need); return SG_ERR_WORKSPACE; }
+    uint32_t* rec = (uint32_t*)((uint8_t*)ws + ((mw + 255) & ~(size_t)255));
+    SG_TRY(merge_pack_run(home, inv, n, omega, k, owner, 0, 1, idmaps, graphs, graphs_d, R, rec, ws, mw, S(stream)));
+    return merge_union_run(home, inv, n, omega, k, owner, 0, idmaps, graphs, graphs_d, R, rec, send, merged, merged_d,
+                           ws, mw, S(stream));
+}
+
+// ------------------------------------------------------------------ a9
+sg_status scalegann_search_workspace(uint64_t n, uint32_t d, sg_dtype dtype, uint32_t nq, uint32_t topk, uint32_t beam,
+                                     size_t* bytes) {
+    SG_CHECK_ARG(bytes, "null bytes");
+    (void)beam;
+    size_t gt = knn_total_ws(nq, n, d, worst_prec(dtype, SG_PREC_AUTO), topk, false) + (size_t)nq * topk * 8 + 512;
+    size_t bs = beam_ws(n, nq) + (size_t)nq * topk * 4 + 1024;
+    *bytes = gt + bs;
+    return SG_OK;
+}
+
+sg_status scalegann_search_eval(const void* x, sg_dtype dtype, uint64_t n, uint32_t d, const uint32_t* graph, uint32_t R,
+                                uint32_t entry, const void* queries, uint32_t nq, uint32_t topk, uint32_t beam,
+                                int32_t metric, const uint32_t* gt, uint32_t* gt_out, uint32_t* out_ids,
+                                double* recall_host, void* ws, size_t ws_bytes, void* stream) {
+    SG_CHECK_ARG(x && graph && queries && out_ids && nq > 0 && n > 0 && d > 0 && d <= 1024, "search: bad arguments");
+    SG_CHECK_ARG(entry < n, "search: entry out of range");
+    SG_CHECK_ARG(R >= 1 && R <= 128 && topk >= 1 && topk <= beam && beam <= 512, "search: need R<=128, topk<=beam<=512");
+    SG_CHECK_ARG(metric == SG_L2 || metric == SG_IP, "search: bad metric");
+    cudaStream_t st = S(stream);
+    Carver cv(ws, ws_bytes);
+    const uint32_t* g = gt;
+    if (!g) {
+        uint32_t* gbuf = gt_out ? gt_out : cv.take<uint32_t>((size_t)nq * topk);
+        float* gd = cv.take<float>((size_t)nq * topk);
+        if (!cv.ok()) { set_error("search: workspace too small"); return SG_ERR_WORKSPACE; }
+        Carver kc = cv;
+        SG_TRY(knn_impl(queries, nullptr, nq, x, nullptr, n, dtype, d, 0, topk, metric, SG_PREC_AUTO, gbuf, gd, nullptr,
+                        kc.base ? kc.base + kc.off : nullptr, kc.cap > kc.off ? kc.cap - kc.off : 0, st));
+        g = gbuf;
+    }
+    SG_TRY(beam_run(x, dtype, n, d, graph, R, entry, queries, nq, topk, beam, metric, out_ids, nullptr, cv, st));
+    if (recall_host) return recall_run(out_ids, g, nq, topk, recall_host, cv, st);
+    return SG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,191 @@
+// Internal helpers of libscalegann.so (CUDA path).  Shares nothing with oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "../../include/scalegann.h"
+
+#define SG_SENT 0xFFFFFFFFu
+
+// ------------------------------------------------------------------ errors
+namespace sg {
+void set_error(const char* fmt, ...);
+sg_status cuda_status(cudaError_t e, const char* what);
+}  // namespace sg
+
+#define SG_CHECK_ARG(cond, ...)              \
+    do {                                     \
+        if (!(cond)) {                       \
+            sg::set_error(__VA_ARGS__);      \
+            return SG_ERR_INVALID_ARG;       \
+        }                                    \
+    } while (0)
+
+#define SG_CUDA(call)                                                  \
+    do {                                                               \
+        cudaError_t _e = (call);                                       \
+        if (_e != cudaSuccess) return sg::cuda_status(_e, #call);      \
+    } while (0)
+
+#define SG_LAUNCHED(name)                                               \
+    do {                                                                \
+        cudaError_t _e = cudaGetLastError();                            \
+        if (_e != cudaSuccess) return sg::cuda_status(_e, name);        \
+    } while (0)
+
+#define SG_TRY(call)                              \
+    do {                                          \
+        sg_status _s = (call);                    \
+        if (_s != SG_OK) return _s;               \
+    } while (0)
+
+namespace sg {
+
+// ------------------------------------------------------------------ workspace
+// Bump allocator over the caller's workspace; used twice: once with base=null
+// to size, once to carve.  256-byte alignment (TMA needs 16, vector loads 16).
+struct Carver {
+    uint8_t* base;
+    size_t cap;
+    size_t off = 0;
+    Carver(void* b, size_t c) : base((uint8_t*)b), cap(c) {}
+    template <class T>
+    T* take(size_t count) {
+        off = (off + 255) & ~(size_t)255;
+        T* p = base ? (T*)(base + off) : nullptr;
+        off += count * sizeof(T);
+        return p;
+    }
+    bool ok() const { return off <= cap; }
+};
+
+inline cudaStream_t S(void* s) { return (cudaStream_t)s; }
+
+inline int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+// ------------------------------------------------------------------ device helpers
+// float -> uint32 with the same total order (ascending); -0 is canonicalised to +0.
+__device__ __forceinline__ uint32_t f2ord(float f) {
+    uint32_t u = __float_as_uint(f + 0.0f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ord2f(uint32_t o) {
+    uint32_t u = (o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o;
+    return __uint_as_float(u);
+}
+
+// Warp-cooperative bitonic sort (ascending) of n = power of two uint64 keys in
+// shared memory, optionally carrying a uint32 payload.  All 32 lanes call it.
+__device__ __forceinline__ void warp_sort_u64(uint64_t* a, uint32_t n, uint32_t lane) {
+    for (uint32_t k = 2; k <= n; k <<= 1) {
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            for (uint32_t i = lane; i < n; i += 32) {
+                uint32_t p = i ^ j;
+                if (p > i) {
+                    uint64_t x = a[i], y = a[p];
+                    bool up = (i & k) == 0;
+                    if ((x > y) == up) { a[i] = y; a[p] = x; }
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
+__device__ __forceinline__ void warp_sort_u64_payload(uint64_t* a, uint32_t* pl, uint32_t n, uint32_t lane) {
+    for (uint32_t k = 2; k <= n; k <<= 1) {
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            for (uint32_t i = lane; i < n; i += 32) {
+                uint32_t p = i ^ j;
+                if (p > i) {
+                    uint64_t x = a[i], y = a[p];
+                    bool up = (i & k) == 0;
+                    if ((x > y) == up) {
+                        a[i] = y; a[p] = x;
+                        uint32_t t = pl[i]; pl[i] = pl[p]; pl[p] = t;
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, uint32_t lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= (uint32_t)o) v += t;
+    }
+    return v;
+}
+
+// Block-wide exclusive scan of one uint32 per thread (blockDim.x <= 1024,
+// multiple of 32); `tmp` holds >= 33 words of shared memory.  Returns the
+// exclusive prefix; *total receives the block sum.
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* tmp, uint32_t* total) {
+    uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    uint32_t inc = warp_incl_scan(v, lane);
+    if (lane == 31) tmp[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        uint32_t s = lane < nw ? tmp[lane] : 0;
+        uint32_t si = warp_incl_scan(s, lane);
+        if (lane < nw) tmp[lane] = si - s;
+        if (lane == 31) tmp[32] = si;
+    }
+    __syncthreads();
+    uint32_t r = tmp[w] + inc - v;
+    if (total) *total = tmp[32];
+    __syncthreads();
+    return r;
+}
+
+}  // namespace sg
+
+// ------------------------------------------------------------------ internal launchers
+// (host functions implemented in the per-stage .cu files, called by api.cu)
+namespace sg {
+// gather.cu
+struct Operand {
+    void* a = nullptr;         // rows_pad x kdim elements (f16 or f32-as-tf32)
+    void* b = nullptr;         // == a unless TF32X3
+    float* norm_a = nullptr;   // rows_pad (0 pad)
+    float* norm_b = nullptr;   // rows_pad (+inf pad for columns)
+    uint32_t kdim = 0;         // padded K in elements
+    uint32_t esize = 2;        // 2 (f16) or 4 (tf32)
+    uint64_t rows = 0, rows_pad = 0;
+};
+// AUTO -> F16_EXACT when every referenced value is an integer with |v| <= 2048 and
+// 2*d*max^2 < 2^24 (then dots, norms and distances are exact in fp32), else TF32.
+int resolve_precision(int32_t precision, sg_dtype dtype, uint32_t d, const void* xa, const uint32_t* ida,
+                      uint64_t ma, const void* xb, const uint32_t* idb, uint64_t mb, unsigned int* flags,
+                      cudaStream_t st, sg_status* err);
+uint32_t operand_kdim(int prec, uint32_t d);
+size_t operand_bytes(int prec, uint32_t d, uint64_t rows);
+sg_status gather_operand(const void* x, sg_dtype dtype, uint32_t d, const uint32_t* ids, uint64_t m,
+                         int prec, int metric, bool as_columns, Carver& cv, Operand* op, cudaStream_t st);
+// knn_tc.cu
+size_t knn_core_workspace(uint32_t L);
+sg_status knn_core(const Operand& A, const Operand& B, int metric, bool self_exclude, uint32_t L,
+                   uint32_t* ids, float* dists, float* probe, Carver& cv, cudaStream_t st);
+// prune.cu / reverse.cu
+sg_status launch_prune(const uint32_t* knn, const float* knn_d, uint64_t m, uint32_t L, uint32_t R,
+                       uint32_t rule, uint32_t* out, float* out_d, cudaStream_t st);
+sg_status launch_reverse(const uint32_t* pruned, const float* pruned_d, uint64_t m, uint32_t R, uint32_t h,
+                         uint32_t* out, float* out_d, Carver& cv, cudaStream_t st);
+// scan.cu
+size_t scan_workspace(uint64_t n);
+sg_status excl_scan_u32_to_u64(const uint32_t* in, uint64_t* out, uint64_t n, Carver& cv, cudaStream_t st);
+}  // namespace sg

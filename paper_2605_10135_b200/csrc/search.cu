@@ -1,0 +1,209 @@
+// a9 — recall evaluation: greedy best-first beam search over the merged graph (PAPER P:507
+// "following DiskANN's search strategy"; reading R14) + recall@k against an exact
+// ground truth computed by the tensor-core kNN (a5 with A = queries, B = dataset).
+//
+// One warp per query.  The pool (<= beam entries, keys (ord(dist) << 32 | id)) stays sorted in
+// shared memory; each expansion takes the lowest unexpanded entry, marks its unvisited
+// neighbours in a per-query visited bitmap (global memory, one bit per vector), computes their
+// distances (lane per neighbour), sorts the new keys and merges them into the pool by rank
+// (binary search in both lists), truncating to beam — the same semantics as sorting the union
+// by (dist, id) and truncating.
+#include "common.cuh"
+
+namespace sg {
+namespace {
+
+constexpr int SW = 4;   // queries (warps) per CTA
+
+struct SearchArgs {
+    const void* x;
+    const void* q;
+    const uint32_t* graph;
+    uint32_t* visited;     // batch x words
+    uint32_t* out_ids;
+    uint64_t n, words;
+    uint32_t d, R, entry, nq, q0, topk, beam, poolcap, newcap;
+    int dtype, metric;
+    unsigned long long* ndist;
+};
+
+__device__ __forceinline__ float qdist(const SearchArgs& a, const float* qv, uint32_t v) {
+    float s = 0.f;
+    if (a.dtype == SG_U8) {
+        const uint8_t* row = (const uint8_t*)a.x + (uint64_t)v * a.d;
+        for (uint32_t j = 0; j < a.d; j++) {
+            const float t = (float)row[j];
+            s = a.metric == SG_IP ? __fmaf_rn(-t, qv[j], s) : __fmaf_rn(t - qv[j], t - qv[j], s);
+        }
+    } else {
+        const float* row = (const float*)a.x + (uint64_t)v * a.d;
+        for (uint32_t j = 0; j < a.d; j++) {
+            const float t = __ldg(row + j);
+            s = a.metric == SG_IP ? __fmaf_rn(-t, qv[j], s) : __fmaf_rn(t - qv[j], t - qv[j], s);
+        }
+    }
+    return s;
+}
+
+__device__ __forceinline__ uint32_t lower_bound_u64(const uint64_t* arr, uint32_t n, uint64_t key) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (arr[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(SW * 32) beam_kernel(SearchArgs a) {
+    extern __shared__ __align__(16) uint8_t sm[];
+    const uint32_t w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t per = (2 * a.poolcap + a.newcap) * 8 + 2 * a.poolcap * 4 + a.d * 4;
+    uint8_t* base = sm + w * per;
+    uint64_t* pool = (uint64_t*)base;
+    uint64_t* pool2 = pool + a.poolcap;
+    uint64_t* nb = pool2 + a.poolcap;
+    uint32_t* ex = (uint32_t*)(nb + a.newcap);
+    uint32_t* ex2 = ex + a.poolcap;
+    float* qv = (float*)(ex2 + a.poolcap);
+    const uint32_t qi = a.q0 + blockIdx.x * SW + w;
+    if (qi >= a.nq) return;
+    uint32_t* vis = a.visited + (uint64_t)(blockIdx.x * SW + w) * a.words;
+    for (uint32_t j = lane; j < a.d; j += 32)
+        qv[j] = a.dtype == SG_U8 ? (float)((const uint8_t*)a.q)[(uint64_t)qi * a.d + j]
+                                 : ((const float*)a.q)[(uint64_t)qi * a.d + j];
+    for (uint64_t i = lane; i < a.words; i += 32) vis[i] = 0;
+    __syncwarp();
+    __threadfence_block();
+    unsigned long long nd = 1;
+    if (lane == 0) {
+        pool[0] = ((uint64_t)f2ord(qdist(a, qv, a.entry)) << 32) | a.entry;
+        ex[0] = 0;
+        vis[a.entry >> 5] |= 1u << (a.entry & 31);
+    }
+    uint32_t np = 1;
+    __syncwarp();
+    while (true) {
+        // lowest unexpanded entry
+        uint32_t u = SG_SENT;
+        for (uint32_t i0 = 0; i0 < np && u == SG_SENT; i0 += 32) {
+            const uint32_t i = i0 + lane;
+            const uint32_t bal = __ballot_sync(0xffffffffu, i < np && ex[i] == 0);
+            if (bal) u = i0 + __ffs(bal) - 1;
+        }
+        if (u == SG_SENT) break;
+        const uint32_t node = (uint32_t)pool[u];
+        __syncwarp();
+        if (lane == 0) ex[u] = 1;
+        // new neighbours
+        uint32_t nn = 0;
+        for (uint32_t j0 = 0; j0 < a.R; j0 += 32) {
+            const uint32_t j = j0 + lane;
+            uint64_t key = 0;
+            bool fresh = false;
+            if (j < a.R) {
+                const uint32_t v = a.graph[(uint64_t)node * a.R + j];
+                if (v != SG_SENT) {
+                    const uint32_t bit = 1u << (v & 31);
+                    fresh = !(atomicOr(&vis[v >> 5], bit) & bit);
+                    if (fresh) key = ((uint64_t)f2ord(qdist(a, qv, v)) << 32) | v;
+                }
+            }
+            const uint32_t bal = __ballot_sync(0xffffffffu, fresh);
+            if (fresh) nb[nn + __popc(bal & ((1u << lane) - 1u))] = key;
+            nn += __popc(bal);
+        }
+        nd += nn;
+        if (nn == 0) { __syncwarp(); continue; }
+        uint32_t p2 = 32;
+        while (p2 < nn) p2 <<= 1;
+        for (uint32_t i = nn + lane; i < p2; i += 32) nb[i] = ~0ull;
+        __syncwarp();
+        warp_sort_u64(nb, p2, lane);
+        // merge pool[0..np) and nb[0..nn) by rank, keep the first `beam`
+        for (uint32_t i = lane; i < np; i += 32) {
+            const uint32_t pos = i + lower_bound_u64(nb, nn, pool[i]);
+            if (pos < a.beam) { pool2[pos] = pool[i]; ex2[pos] = ex[i]; }
+        }
+        for (uint32_t j = lane; j < nn; j += 32) {
+            const uint32_t pos = j + lower_bound_u64(pool, np, nb[j]);
+            if (pos < a.beam) { pool2[pos] = nb[j]; ex2[pos] = 0; }
+        }
+        np = min(a.beam, np + nn);
+        __syncwarp();
+        for (uint32_t i = lane; i < np; i += 32) { pool[i] = pool2[i]; ex[i] = ex2[i]; }
+        __syncwarp();
+    }
+    for (uint32_t i = lane; i < a.topk; i += 32)
+        a.out_ids[(uint64_t)qi * a.topk + i] = i < np ? (uint32_t)pool[i] : SG_SENT;
+    if (lane == 0 && a.ndist) atomicAdd(a.ndist, nd);
+}
+
+__global__ void recall_kernel(const uint32_t* __restrict__ ret, const uint32_t* __restrict__ gt, uint32_t nq,
+                              uint32_t topk, unsigned long long* hits) {
+    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    unsigned long long h = 0;
+    for (uint32_t i = 0; i < topk; i++) {
+        const uint32_t r = ret[(uint64_t)q * topk + i];
+        if (r == SG_SENT) continue;
+        for (uint32_t j = 0; j < topk; j++) if (gt[(uint64_t)q * topk + j] == r) { h++; break; }
+    }
+    atomicAdd(hits, h);
+}
+
+}  // namespace
+
+static uint32_t pow2_at_least(uint32_t v) { uint32_t p = 32; while (p < v) p <<= 1; return p; }
+
+size_t beam_ws(uint64_t n, uint32_t nq) {
+    const uint64_t words = (n + 31) / 32;
+    uint64_t batch = (1ull << 30) / (words * 4 + 1);
+    if (batch < SW) batch = SW;
+    if (batch > nq) batch = (nq + SW - 1) / SW * SW;
+    return batch * words * 4 + 4096;
+}
+
+sg_status beam_run(const void* x, sg_dtype dtype, uint64_t n, uint32_t d, const uint32_t* graph, uint32_t R,
+                   uint32_t entry, const void* q, uint32_t nq, uint32_t topk, uint32_t beam, int metric,
+                   uint32_t* out_ids, unsigned long long* ndist, Carver& cv, cudaStream_t st) {
+    const uint64_t words = (n + 31) / 32;
+    uint64_t batch = (1ull << 30) / (words * 4 + 1);
+    if (batch < SW) batch = SW;
+    if (batch > nq) batch = (nq + SW - 1) / SW * SW;
+    batch = batch / SW * SW;
+    uint32_t* vis = cv.take<uint32_t>(batch * words);
+    if (!cv.ok()) { set_error("search: workspace too small"); return SG_ERR_WORKSPACE; }
+    SearchArgs a{};
+    a.x = x; a.q = q; a.graph = graph; a.visited = vis; a.out_ids = out_ids; a.n = n; a.words = words;
+    a.d = d; a.R = R; a.entry = entry; a.nq = nq; a.topk = topk; a.beam = beam;
+    a.poolcap = pow2_at_least(beam + R);
+    a.newcap = pow2_at_least(R);
+    a.dtype = dtype; a.metric = metric; a.ndist = ndist;
+    const size_t per = (2 * a.poolcap + a.newcap) * 8 + 2 * a.poolcap * 4 + d * 4;
+    const size_t smem = per * SW;
+    SG_CHECK_ARG(smem <= 200 * 1024, "search: beam/R/d too large for shared memory");
+    SG_CUDA(cudaFuncSetAttribute(beam_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    for (uint64_t q0 = 0; q0 < nq; q0 += batch) {
+        a.q0 = (uint32_t)q0;
+        const uint64_t cnt = batch < nq - q0 ? batch : nq - q0;
+        beam_kernel<<<(unsigned)((cnt + SW - 1) / SW), SW * 32, smem, st>>>(a);
+        SG_LAUNCHED("beam_kernel");
+    }
+    return SG_OK;
+}
+
+sg_status recall_run(const uint32_t* ret, const uint32_t* gt, uint32_t nq, uint32_t topk, double* recall_host,
+                     Carver& cv, cudaStream_t st) {
+    unsigned long long* hits = cv.take<unsigned long long>(1);
+    if (!cv.ok()) { set_error("search: workspace too small"); return SG_ERR_WORKSPACE; }
+    SG_CUDA(cudaMemsetAsync(hits, 0, sizeof(unsigned long long), st));
+    recall_kernel<<<(nq + 255) / 256, 256, 0, st>>>(ret, gt, nq, topk, hits);
+    SG_LAUNCHED("recall_kernel");
+    unsigned long long h = 0;
+    SG_CUDA(cudaMemcpyAsync(&h, hits, sizeof(h), cudaMemcpyDeviceToHost, st));
+    SG_CUDA(cudaStreamSynchronize(st));
+    *recall_host = nq ? (double)h / ((double)nq * topk) : 0.0;
+    return SG_OK;
+}
+
+}  // namespace sg
