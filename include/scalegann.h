@@ -68,7 +68,7 @@ typedef struct {
     uint32_t theta0_ppm;   /* base replica fraction theta0 in ppm (R4), default 400000 */
     float alpha;           /* tau_b = 1 + alpha/(1+b) (R5), default 1.0 */
     uint32_t block_size;   /* vectors per block, default 65536 */
-    uint64_t capacity;     /* max vectors per cluster; 0 = derive (R9) */
+    uint64_t capacity;     /* max vectors per cluster; 0 = derive ceil(1.15 ceil(n/(k(1-theta0)))) (R9) */
 } sg_partition_params;
 
 typedef struct {

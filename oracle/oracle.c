@@ -230,11 +230,15 @@ void oracle_centroid_dist(const void* x, int dtype, uint64_t n, uint32_t d, cons
 }
 
 /* ------------------------------------------------------------------ P2/P3 */
-/* capacity = ceil(1.15 * ceil(n (1 + theta0) / k)) in integers (reading R9,
- * SPEC S:242). */
+/* capacity = ceil(1.15 * ceil(n / (k (1 - theta0)))) in integers (reading R9).
+ * Replicas may take up to theta0*cap of a cluster (budget, R4), so this sizing keeps
+ * k*cap*(1-theta0) >= 1.15 n: room for every original vector is always left, as P:307
+ * requires ("each cluster must reserve capacity for original vectors processed later") and
+ * SPEC S:182 states as an invariant.  SPEC S:242's ceil(1.15*ceil(n(1+theta0)/k)) does not
+ * guarantee it (replicas can exhaust it: SG_ERR_CAPACITY on clustered data). */
 uint64_t oracle_capacity(uint64_t n, uint32_t k, uint32_t theta0_ppm) {
-    unsigned __int128 num = (unsigned __int128)(1000000u + theta0_ppm) * n;
-    unsigned __int128 den = (unsigned __int128)1000000u * k;
+    unsigned __int128 num = (unsigned __int128)1000000u * n;
+    unsigned __int128 den = (unsigned __int128)(1000000u - theta0_ppm) * k;
     unsigned __int128 base = (num + den - 1) / den;
     return (uint64_t)((base * 115 + 99) / 100);
 }

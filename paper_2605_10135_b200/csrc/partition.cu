@@ -255,8 +255,8 @@ __global__ void __launch_bounds__(K2_THREADS, 1) assign_kernel(PartArgs a) {
 }  // namespace
 
 uint64_t derive_capacity(uint64_t n, uint32_t k, uint32_t t) {
-    unsigned __int128 num = (unsigned __int128)(1000000u + t) * n;
-    unsigned __int128 den = (unsigned __int128)1000000u * k;
+    unsigned __int128 num = (unsigned __int128)1000000u * n;
+    unsigned __int128 den = (unsigned __int128)(1000000u - t) * k;
     unsigned __int128 base = (num + den - 1) / den;
     return (uint64_t)((base * 115 + 99) / 100);
 }

@@ -156,7 +156,7 @@ def test_partition_bit_exact(api, oracle_mod, block, kind):
 def test_partition_capacity_binding_and_omega3(api, oracle_mod):
     x = _clustered(6000, 16, seed=9)
     C = x[:6].clone()                      # poor centroids -> capacity binds
-    for omega, cap in ((3, 0), (2, 1400)):
+    for omega, cap in ((3, 0), (2, 1700)):
         home, pd, counts = api.scalegann_partition(x.cuda(), C.cuda(), omega=omega, epsilon=1.5, block_size=500,
                                                    capacity=cap)
         r = oracle_mod.partition(x.numpy(), C.numpy(), omega=omega, eps=1.5, block_size=500, capacity=cap)

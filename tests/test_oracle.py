@@ -47,13 +47,19 @@ def test_p1_fma_chain_order(oracle_mod):
 
 
 # ---------------------------------------------------------------- P2/P3 ----
-def test_capacity_closed_form(oracle_mod):
-    # SPEC S:242 cap = ceil(1.15 * ceil(n (1+theta0) / k)), theta0 = 0.4
-    assert oracle_mod.capacity(10_000, 2) == 8050
-    assert oracle_mod.capacity(1_000_000, 4) == 402_500
-    assert oracle_mod.capacity(10_000_000, 8) == 2_012_500
-    assert oracle_mod.capacity(5_000_000, 8) == 1_006_250
-    assert oracle_mod.capacity(100_000_000, 8) == 20_125_000
+def test_capacity_reading_r9(oracle_mod):
+    # R9: cap = ceil(1.15 * ceil(n / (k (1 - theta0)))), theta0 = 0.4; values worked by hand:
+    # C0 10000/(2*0.6) = 8333.3 -> 8334 -> 9584.1 -> 9585, C1 416666.7 -> 416667 -> 479168, ...
+    assert oracle_mod.capacity(10_000, 2) == 9585
+    assert oracle_mod.capacity(1_000_000, 4) == 479_168
+    assert oracle_mod.capacity(10_000_000, 8) == 2_395_835
+    assert oracle_mod.capacity(5_000_000, 8) == 1_197_918
+    assert oracle_mod.capacity(100_000_000, 8) == 23_958_335
+    # the property the reading exists for: with every replica budget at its
+    # cap theta0*cap, the clusters still hold 1.15 n originals
+    for n, k in ((10_000, 2), (1_000_000, 4), (12_345_677, 7), (3, 3)):
+        cap = oracle_mod.capacity(n, k)
+        assert k * cap * 0.6 >= 1.15 * n
 
 
 def test_budget_rule(oracle_mod):
