@@ -237,6 +237,14 @@ sg_status scalegann_gemm_probe(const void* xa, uint64_t ma, const void* xb, uint
                                uint32_t d, int32_t precision, float* out, void* ws, size_t ws_bytes,
                                void* stream);
 
+/* Kernel accounting for the benchmark: every kernel launch of this library increments a
+ * counter; with stats enabled, CUDA events are recorded on the launching stream around each
+ * distance-kernel launch (a5).  scalegann_stats_read synchronises those events and returns
+ * the summed device time, the number of distance launches and of all launches since the last
+ * reset. */
+sg_status scalegann_stats_enable(int on);
+sg_status scalegann_stats_read(double* knn_ms, uint64_t* knn_launches, uint64_t* kernel_launches, int reset);
+
 #ifdef __cplusplus
 }
 #endif

@@ -47,7 +47,7 @@ EXPORTS = [
     "scalegann_prune", "scalegann_reverse_workspace", "scalegann_reverse", "scalegann_build_shard_workspace",
     "scalegann_build_shard", "scalegann_optimize_from_knn", "scalegann_merge_counts", "scalegann_merge_workspace",
     "scalegann_merge_pack", "scalegann_merge_union", "scalegann_merge", "scalegann_search_workspace",
-    "scalegann_search_eval", "scalegann_gemm_probe",
+    "scalegann_search_eval", "scalegann_gemm_probe", "scalegann_stats_enable", "scalegann_stats_read",
 ]
 
 
@@ -101,6 +101,8 @@ def load(build_if_missing: bool = True):
         "scalegann_search_eval": ([vp, i32, u64, u32, vp, u32, u32, vp, u32, u32, u32, i32, vp, vp, vp,
                                    P(ctypes.c_double), vp, sz, vp], i32),
         "scalegann_gemm_probe": ([vp, u64, vp, u64, i32, u32, i32, vp, vp, sz, vp], i32),
+        "scalegann_stats_enable": ([ctypes.c_int], i32),
+        "scalegann_stats_read": ([P(ctypes.c_double), pu64, pu64, ctypes.c_int], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -389,6 +391,20 @@ def scalegann_merge(home, inv, idmaps, graphs, graphs_d, ws=None):
     _check(L.scalegann_merge(_ptr(home), _ptr(inv), n, omega, k, _ptr_array(idmaps, k), _ptr_array(graphs, k),
                              _ptr_array(graphs_d, k), R, _ptr(merged), _ptr(merged_d), p, nbytes, _stream()))
     return merged, merged_d
+
+
+# ----------------------------------------------------------------------------- diagnostics
+def scalegann_stats_enable(on=True):
+    _check(load().scalegann_stats_enable(int(on)))
+
+
+def scalegann_stats_read(reset=True):
+    """(distance-kernel device ms, distance launches, all kernel launches) since the last reset."""
+    ms = ctypes.c_double(0)
+    kl = ctypes.c_uint64(0)
+    al = ctypes.c_uint64(0)
+    _check(load().scalegann_stats_read(ctypes.byref(ms), ctypes.byref(kl), ctypes.byref(al), int(reset)))
+    return ms.value, kl.value, al.value
 
 
 # ----------------------------------------------------------------------------- a9

@@ -3,6 +3,9 @@
 // step of the path runs in this library's kernels.
 #include <stdarg.h>
 
+#include <utility>
+#include <vector>
+
 #include "common.cuh"
 
 namespace sg {
@@ -41,6 +44,33 @@ sg_status recall_run(const uint32_t* ret, const uint32_t* gt, uint32_t nq, uint3
                      Carver& cv, cudaStream_t st);
 
 static thread_local char g_err[512] = "";
+
+// ---- diagnostics: launch counter + event timing of the distance kernel
+struct Stats {
+    bool on = false;
+    uint64_t launches = 0, knn_launches = 0;
+    cudaEvent_t pending_begin = nullptr;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> knn;
+};
+static Stats g_stats;
+
+void note_launch() { g_stats.launches++; }
+
+void knn_time_begin(cudaStream_t st) {
+    g_stats.knn_launches++;
+    if (!g_stats.on) return;
+    cudaEventCreate(&g_stats.pending_begin);
+    cudaEventRecord(g_stats.pending_begin, st);
+}
+
+void knn_time_end(cudaStream_t st) {
+    if (!g_stats.on || !g_stats.pending_begin) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    g_stats.knn.emplace_back(g_stats.pending_begin, e);
+    g_stats.pending_begin = nullptr;
+}
 
 void set_error(const char* fmt, ...) {
     va_list ap;
@@ -88,6 +118,31 @@ extern "C" {
 
 int scalegann_abi_version(void) { return SCALEGANN_ABI_VERSION; }
 const char* scalegann_last_error(void) { return g_err; }
+
+sg_status scalegann_stats_enable(int on) {
+    g_stats.on = on != 0;
+    return SG_OK;
+}
+
+sg_status scalegann_stats_read(double* knn_ms, uint64_t* knn_launches, uint64_t* kernel_launches, int reset) {
+    double ms = 0;
+    for (auto& pr : g_stats.knn) {
+        float t = 0;
+        SG_CUDA(cudaEventSynchronize(pr.second));
+        SG_CUDA(cudaEventElapsedTime(&t, pr.first, pr.second));
+        ms += t;
+    }
+    if (knn_ms) *knn_ms = ms;
+    if (knn_launches) *knn_launches = g_stats.knn_launches;
+    if (kernel_launches) *kernel_launches = g_stats.launches;
+    if (reset) {
+        for (auto& pr : g_stats.knn) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
+        g_stats.knn.clear();
+        g_stats.knn_launches = 0;
+        g_stats.launches = 0;
+    }
+    return SG_OK;
+}
 
 // ------------------------------------------------------------------ a1
 sg_status scalegann_kmeans_workspace(uint64_t n, uint32_t d, uint32_t k, uint32_t spc, size_t* bytes) {

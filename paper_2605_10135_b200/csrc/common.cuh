@@ -33,7 +33,15 @@ sg_status cuda_status(cudaError_t e, const char* what);
     do {                                                                \
         cudaError_t _e = cudaGetLastError();                            \
         if (_e != cudaSuccess) return sg::cuda_status(_e, name);        \
+        sg::note_launch();                                              \
     } while (0)
+
+namespace sg {
+// diagnostics (api.cu): kernel launch counter and CUDA-event timing of the distance kernel
+void note_launch();
+void knn_time_begin(cudaStream_t st);
+void knn_time_end(cudaStream_t st);
+}  // namespace sg
 
 #define SG_TRY(call)                              \
     do {                                          \

@@ -451,8 +451,10 @@ sg_status launch_t(const CUtensorMap& a, const CUtensorMap& b, KnnParams& p, cud
     auto kern = knn_tc_kernel<KIND, NKA, EPL>;
     SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const uint32_t grid = p.n_rb < (uint32_t)num_sms() ? p.n_rb : (uint32_t)num_sms();
+    knn_time_begin(st);
     kern<<<grid, NTHREADS, smem, st>>>(a, b, p);
     SG_LAUNCHED("knn_tc_kernel");
+    knn_time_end(st);
     return SG_OK;
 }
 
