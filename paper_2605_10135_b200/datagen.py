@@ -10,11 +10,15 @@ lines 391-416: Sift 128-d uint8, Deep 96-d float, Laion 768-d float) and the
 recipe of SURVEY.md §8(d) "Generator parameters":
 
 * Gaussian mixture with ``K_MIX = 1024`` components of uniform weight, centres
-  ``mu_c ~ N(0, I)``; a point is ``mu_c + 0.35 * sqrt(lambda) * z`` with
+  ``mu_c ~ N(0, I)``; a point is ``mu_c + 1.5 * sqrt(lambda) * z`` with
   ``lambda_i = i^-beta`` normalised to mean 1 (beta 0.3 SIFT-like, 0.7
   DEEP-like, 1.0 text-like).
-* SIFT-shaped (C1 float, C4 uint8): ``clip(round(45.7 * max(0, x + 0.4)), 0, 255)``
-  which gives ~36% zeros and mean norm ~512, integer valued.
+* SIFT-shaped (C1 float, C4 uint8): ``clip(round(30 * max(0, x + 0.4)), 0, 255)``
+  which gives ~41% zeros and mean norm ~512, integer valued.  The spread 1.5 (not the
+  0.35 SURVEY §8(d) proposed) makes neighbouring components overlap as real descriptors do:
+  at 0.35 the ~1000 points per component of a 1M dataset form disjoint exact-kNN graphs
+  (one strong component per mixture component, recall@10 ~ 0.06 even for the oracle-built
+  graph); at 1.5 the graph is connected and the oracle-built graph reaches recall ~0.99.
 * DEEP/text-shaped: rows L2-normalised.
 * C0: iid N(0, 1).
 
@@ -30,8 +34,8 @@ import dataclasses
 import torch
 
 K_MIX = 1024
-SPREAD = 0.35
-SIFT_SCALE = 45.7
+SPREAD = 1.5
+SIFT_SCALE = 30.0
 SIFT_OFFSET = 0.4
 CHUNK = 1 << 20
 DATA_SEED = 0x5CA1E

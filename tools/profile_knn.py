@@ -1,0 +1,47 @@
+"""Run the a5 distance kernel alone on one synthetic shard (for ncu / quick timing).
+
+    python tools/profile_knn.py --m 400000 --L 128 [--reps 3] [--kind sift|gauss]
+Prints device time per launch (CUDA events on the launching stream) and achieved TFLOP/s
+(algorithmic 2*m^2*d).
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_2605_10135_b200 import api, datagen  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--m", type=int, default=400_000)
+    ap.add_argument("--d", type=int, default=128)
+    ap.add_argument("--L", type=int, default=128)
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--kind", default="sift")
+    ap.add_argument("--precision", type=int, default=0)
+    a = ap.parse_args()
+    api.load()
+    x = (datagen.sift_like(a.m, a.d, device="cuda") if a.kind == "sift"
+         else datagen.gaussian(a.m, a.d, device="cuda"))
+    ws = api.Workspace()
+    api.scalegann_knn(x, a.L, precision=a.precision, ws=ws)   # warm-up
+    torch.cuda.synchronize()
+    api.scalegann_stats_read(reset=True)
+    api.scalegann_stats_enable(True)
+    for _ in range(a.reps):
+        api.scalegann_knn(x, a.L, precision=a.precision, ws=ws)
+    torch.cuda.synchronize()
+    ms, nl, _ = api.scalegann_stats_read(reset=True)
+    per = ms / max(nl, 1)
+    fl = 2.0 * a.m * a.m * a.d
+    print(json.dumps({"m": a.m, "d": a.d, "L": a.L, "ms_per_launch": per, "tflops": fl / (per / 1e3) / 1e12}))
+
+
+if __name__ == "__main__":
+    main()
