@@ -30,7 +30,8 @@ namespace sg {
 namespace {
 
 constexpr uint32_t BM = 128, BN = 128, ATOM = 128 * 128;   // bytes per swizzle atom (128 rows x 128 B)
-constexpr uint32_t NTHREADS = 192;
+constexpr uint32_t NEPI = 8;                          // epilogue warps
+constexpr uint32_t NTHREADS = 64 + NEPI * 32;
 constexpr uint32_t MAX_STAGES = 12;
 
 // ----------------------------------------------------------------- PTX wrappers
@@ -59,6 +60,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
             : "r"(a), "r"(parity)
             : "memory");
     }
+}
+// same, but lets the waiting thread sleep in hardware until the phase completes (bounded hint)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity) {
+    uint32_t ok = 0;
+    const uint32_t a = smem_u32(b);
+    while (!ok) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(a), "r"(parity), "r"(1000000u)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1) {
     asm volatile(
@@ -99,6 +117,25 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
           "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
         : "r"(taddr));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+          "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+          "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+          "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ uint32_t tmem_ld1(uint32_t taddr) {
+    uint32_t v;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    return v;
 }
 
 // Shared-memory matrix descriptor: K-major, 128-byte swizzle, 8-row core groups 1024 B apart.
@@ -197,17 +234,18 @@ __device__ uint32_t select_L(uint64_t* rb, uint32_t cnt, uint32_t L, uint32_t* h
     return mk;
 }
 
-template <int EPL>
-__device__ void finish_row(uint64_t* rb, uint32_t cnt, uint32_t L, uint32_t* hist, uint64_t* sortbuf,
-                           float na, uint32_t* out_ids, float* out_d, uint32_t lane) {
-    if (cnt > L) { select_L<EPL>(rb, cnt, L, hist, lane); cnt = L; }
+// Merge the two column halves' survivors of one row (each <= L, any order), sort by
+// (dist, id) with dist = |a_i|^2 + key, write the first L (sentinel / +inf padding).
+__device__ void finish_row(const uint64_t* b0, uint32_t c0, const uint64_t* b1, uint32_t c1, uint32_t L,
+                           uint64_t* sortbuf, float na, uint32_t* out_ids, float* out_d, uint32_t lane) {
+    const uint32_t cnt = c0 + c1;
     uint32_t np = 32;
-    while (np < L) np <<= 1;
+    while (np < cnt) np <<= 1;
     for (uint32_t p = lane; p < np; p += 32) {
         uint64_t w = ~0ull;
         if (p < cnt) {
-            uint64_t e = rb[p];
-            float dist = na + ord2f((uint32_t)(e >> 32));
+            const uint64_t e = p < c0 ? b0[p] : b1[p - c0];
+            const float dist = na + ord2f((uint32_t)(e >> 32));
             w = ((uint64_t)f2ord(dist) << 32) | (uint32_t)e;
         }
         sortbuf[p] = w;
@@ -215,7 +253,7 @@ __device__ void finish_row(uint64_t* rb, uint32_t cnt, uint32_t L, uint32_t* his
     __syncwarp();
     warp_sort_u64(sortbuf, np, lane);
     for (uint32_t p = lane; p < L; p += 32) {
-        uint64_t w = sortbuf[p];
+        const uint64_t w = sortbuf[p];
         out_ids[p] = p < cnt ? (uint32_t)w : SG_SENT;
         out_d[p] = p < cnt ? ord2f((uint32_t)(w >> 32)) : __int_as_float(0x7f800000);
     }
@@ -228,21 +266,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, KnnParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint8_t* sA = smem;                                  // NKA atoms
-    uint8_t* sB = smem + NKA * ATOM;                     // stages atoms
+    uint8_t* sA = smem;                                   // NKA atoms
+    uint8_t* sB = smem + NKA * ATOM;                      // stages atoms
     Bars* bars = (Bars*)(sB + p.stages * ATOM);
-    uint32_t* hist_all = (uint32_t*)(bars + 1);          // 4 x 256
-    uint64_t* sort_all = (uint64_t*)(hist_all + 4 * 256);// 4 x 256
+    uint32_t* hist_all = (uint32_t*)(bars + 1);           // NEPI x 256
+    uint64_t* sort_all = (uint64_t*)(hist_all + NEPI * 256);   // NEPI x 512
+    uint32_t* s_cnt = (uint32_t*)(sort_all + NEPI * 512);      // 2 halves x 128 rows
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr uint32_t EL = KIND ? 4 : 2;                // bytes per element
-    constexpr uint32_t ATOM_K = 128 / EL;                // elements per atom along K
+    constexpr uint32_t EL = KIND ? 4 : 2;                 // bytes per element
+    constexpr uint32_t ATOM_K = 128 / EL;                 // elements per atom along K
 
     if (threadIdx.x == 0) {
         for (uint32_t s = 0; s < p.stages; s++) { mbar_init(&bars->full[s], 1); mbar_init(&bars->empty[s], 1); }
         mbar_init(&bars->a_full, 1);
         mbar_init(&bars->a_empty, 1);
-        for (int b = 0; b < 2; b++) { mbar_init(&bars->tm_full[b], 1); mbar_init(&bars->tm_empty[b], 4); }
+        for (int b = 0; b < 2; b++) { mbar_init(&bars->tm_full[b], 1); mbar_init(&bars->tm_empty[b], NEPI); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -265,12 +304,12 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         if (lane == 0) {
             uint32_t stage = 0, sph = 0, it = 0;
             for (uint32_t rb = blockIdx.x; rb < p.n_rb; rb += gridDim.x, it++) {
-                if (it > 0) mbar_wait(&bars->a_empty, (it - 1) & 1);
+                if (it > 0) mbar_wait_sleep(&bars->a_empty, (it - 1) & 1);
                 mbar_expect_tx(&bars->a_full, NKA * ATOM);
                 for (int ka = 0; ka < NKA; ka++) tma_load_2d(&tmA, &bars->a_full, sA + ka * ATOM, ka * ATOM_K, rb * BM);
                 for (uint32_t t = 0; t < p.n_ct; t++) {
                     for (int ka = 0; ka < NKA; ka++) {
-                        mbar_wait(&bars->empty[stage], sph ^ 1);
+                        mbar_wait_sleep(&bars->empty[stage], sph ^ 1);
                         mbar_expect_tx(&bars->full[stage], ATOM);
                         tma_load_2d(&tmB, &bars->full[stage], sB + stage * ATOM, ka * ATOM_K, t * BN);
                         if (++stage == p.stages) { stage = 0; sph ^= 1; }
@@ -285,15 +324,15 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
             uint32_t stage = 0, sph = 0, it = 0, git = 0;
             for (uint32_t rb = blockIdx.x; rb < p.n_rb; rb += gridDim.x, it++) {
-                mbar_wait(&bars->a_full, it & 1);
+                mbar_wait_sleep(&bars->a_full, it & 1);
                 tc_fence_after();
                 for (uint32_t t = 0; t < p.n_ct; t++, git++) {
                     const uint32_t buf = git & 1;
-                    mbar_wait(&bars->tm_empty[buf], ((git >> 1) & 1) ^ 1);
+                    mbar_wait_sleep(&bars->tm_empty[buf], ((git >> 1) & 1) ^ 1);
                     tc_fence_after();
                     const uint32_t dcol = tmem + buf * BN;
                     for (int ka = 0; ka < NKA; ka++) {
-                        mbar_wait(&bars->full[stage], sph);
+                        mbar_wait_sleep(&bars->full[stage], sph);
                         tc_fence_after();
 #pragma unroll
                         for (uint32_t kk = 0; kk < 4; kk++) {
@@ -311,14 +350,17 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         }
     } else {
         // ===================== epilogue: fused distance + top-L =====================
-        const uint32_t q = warp & 3;                       // TMEM lane quadrant
-        const uint32_t r = q * 32 + lane;                  // row within the block
-        uint32_t* hist = hist_all + (warp - 2) * 256;
-        uint64_t* sortbuf = sort_all + (warp - 2) * 256;
+        // warp e = warp-2 in 0..7: TMEM lane quadrant q (rows q*32..), column half h (64 cols)
+        const uint32_t e = warp - 2, q = warp & 3, h = e >> 2;
+        const uint32_t r = q * 32 + lane;                   // row within the block
+        uint32_t* hist = hist_all + e * 256;
+        uint64_t* sortbuf = sort_all + e * 512;
         const uint32_t C = p.C;
-        uint64_t* myrow = p.cand + ((uint64_t)blockIdx.x * BM + r) * C;
-        uint64_t* warprows = p.cand + ((uint64_t)blockIdx.x * BM + q * 32) * C;
+        uint64_t* half_base = p.cand + ((uint64_t)blockIdx.x * 2 + h) * BM * C;
+        uint64_t* myrow = half_base + (uint64_t)r * C;
+        uint64_t* warprows = half_base + (uint64_t)q * 32 * C;
         const float INF = __int_as_float(0x7f800000);
+        const uint32_t tl = tmem + ((q * 32) << 16) + h * 64;
         uint32_t git = 0;
         for (uint32_t rb = blockIdx.x; rb < p.n_rb; rb += gridDim.x) {
             const uint32_t row = rb * BM + r;
@@ -327,11 +369,23 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             uint32_t cnt = 0;
             for (uint32_t t = 0; t < p.n_ct; t++, git++) {
                 const uint32_t buf = git & 1;
-                mbar_wait(&bars->tm_full[buf], (git >> 1) & 1);
+                mbar_wait_sleep(&bars->tm_full[buf], (git >> 1) & 1);
                 tc_fence_after();
+                const uint32_t tb = tl + buf * BN;
+                uint32_t v[2][32];
+                tmem_ld32_nowait(tb, v[0]);
+                tmem_ld32_nowait(tb + 32, v[1]);
+                tmem_wait_ld();
                 const bool diag = p.self_exclude && t == rb;
-#pragma unroll 1
-                for (uint32_t ch = 0; ch < 4; ch++) {
+#pragma unroll
+                for (uint32_t ch = 0; ch < 2; ch++) {
+                    const uint32_t col0 = t * BN + h * 64 + ch * 32;
+                    if (p.probe) {
+                        if (valid)
+                            for (int j = 0; j < 32; j++)
+                                if (col0 + j < p.mb) p.probe[(uint64_t)row * p.mb + col0 + j] = __uint_as_float(v[ch][j]);
+                        continue;
+                    }
                     // make room: rows whose buffer cannot take another 32 candidates are compacted
                     uint32_t need = __ballot_sync(0xffffffffu, cnt > C - 32);
                     while (need) {
@@ -341,60 +395,60 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                         uint32_t kth = select_L<EPL>(warprows + (uint64_t)o * C, c_o, p.L, hist, lane);
                         if (lane == (uint32_t)o) { cnt = p.L; thr = ord2f(kth); }
                     }
-                    uint32_t v[32];
-                    tmem_ld32(tmem + ((q * 32) << 16) + buf * BN + ch * 32, v);
-                    if (ch == 3) {
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(&bars->tm_empty[buf]);
-                    }
-                    const uint32_t col0 = t * BN + ch * 32;
-                    if (p.probe) {
-                        if (valid)
-                            for (int j = 0; j < 32; j++)
-                                if (col0 + j < p.mb) p.probe[(uint64_t)row * p.mb + col0 + j] = __uint_as_float(v[j]);
-                        continue;
-                    }
-                    float key[32];
                     const float4* nb4 = (const float4*)(p.norm_b + col0);
+                    uint32_t mask = 0;
 #pragma unroll
-                    for (int j = 0; j < 8; j++) {
-                        float4 nb = __ldg(nb4 + j);
-                        key[4 * j + 0] = fmaf(p.scale, __uint_as_float(v[4 * j + 0]), nb.x);
-                        key[4 * j + 1] = fmaf(p.scale, __uint_as_float(v[4 * j + 1]), nb.y);
-                        key[4 * j + 2] = fmaf(p.scale, __uint_as_float(v[4 * j + 2]), nb.z);
-                        key[4 * j + 3] = fmaf(p.scale, __uint_as_float(v[4 * j + 3]), nb.w);
+                    for (int j4 = 0; j4 < 8; j4++) {
+                        const float4 nb = __ldg(nb4 + j4);
+                        const float k0 = fmaf(p.scale, __uint_as_float(v[ch][4 * j4 + 0]), nb.x);
+                        const float k1 = fmaf(p.scale, __uint_as_float(v[ch][4 * j4 + 1]), nb.y);
+                        const float k2 = fmaf(p.scale, __uint_as_float(v[ch][4 * j4 + 2]), nb.z);
+                        const float k3 = fmaf(p.scale, __uint_as_float(v[ch][4 * j4 + 3]), nb.w);
+                        mask |= (k0 < thr ? 1u : 0u) << (4 * j4 + 0);
+                        mask |= (k1 < thr ? 1u : 0u) << (4 * j4 + 1);
+                        mask |= (k2 < thr ? 1u : 0u) << (4 * j4 + 2);
+                        mask |= (k3 < thr ? 1u : 0u) << (4 * j4 + 3);
                     }
-                    if (diag && ch == q) {
-#pragma unroll
-                        for (int j = 0; j < 32; j++)
-                            if ((uint32_t)j == lane) key[j] = INF;
-                    }
-                    float mn = key[0];
-#pragma unroll
-                    for (int j = 1; j < 32; j++) mn = fminf(mn, key[j]);
-                    if (mn < thr) {
-#pragma unroll
-                        for (int j = 0; j < 32; j++) {
-                            if (key[j] < thr) {
-                                myrow[cnt] = ((uint64_t)f2ord(key[j]) << 32) | (col0 + j);
-                                cnt++;
-                            }
+                    if (diag && ch + 2 * h == q) mask &= ~(1u << lane);   // self column
+                    // rare path: walk the union of passing columns (warp-uniform), re-read each
+                    // column from TMEM (uniform address) and append where this row passes
+                    uint32_t U = __reduce_or_sync(0xffffffffu, mask);
+                    while (U) {
+                        const uint32_t c = __ffs(U) - 1;
+                        U &= U - 1;
+                        const uint32_t raw = tmem_ld1(tb + ch * 32 + c);
+                        if ((mask >> c) & 1u) {
+                            const float kv = fmaf(p.scale, __uint_as_float(raw), __ldg(p.norm_b + col0 + c));
+                            myrow[cnt] = ((uint64_t)f2ord(kv) << 32) | (col0 + c);
+                            cnt++;
                         }
                     }
                 }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->tm_empty[buf]);
             }
             if (p.probe) continue;
-            // final: exact top-L of every row of this warp, sorted by (dist, id)
+            // ---- final: each half keeps its exact top-L, then the two halves of a row are merged
             __syncwarp();
             for (uint32_t o = 0; o < 32; o++) {
-                const uint32_t c_o = __shfl_sync(0xffffffffu, cnt, o);
-                const uint32_t row_o = rb * BM + q * 32 + o;
-                if (row_o >= p.ma) continue;
-                const float na = p.norm_a[row_o];
-                finish_row<EPL>(warprows + (uint64_t)o * C, c_o, p.L, hist, sortbuf, na,
-                                p.out_ids + (uint64_t)row_o * p.L, p.out_d + (uint64_t)row_o * p.L, lane);
+                uint32_t c_o = __shfl_sync(0xffffffffu, cnt, o);
+                if (c_o > p.L) { select_L<EPL>(warprows + (uint64_t)o * C, c_o, p.L, hist, lane); c_o = p.L; }
+                if (lane == 0) s_cnt[h * BM + q * 32 + o] = c_o;
             }
+            __syncwarp();
+            named_bar_sync(1 + q, 64);
+            for (uint32_t i = 0; i < 16; i++) {
+                const uint32_t rr = q * 32 + h * 16 + i;
+                const uint32_t row_o = rb * BM + rr;
+                if (row_o >= p.ma) continue;
+                const uint32_t c0 = s_cnt[rr], c1 = s_cnt[BM + rr];
+                const uint64_t* b0 = p.cand + ((uint64_t)blockIdx.x * 2 + 0) * BM * C + (uint64_t)rr * C;
+                const uint64_t* b1 = p.cand + ((uint64_t)blockIdx.x * 2 + 1) * BM * C + (uint64_t)rr * C;
+                finish_row(b0, c0, b1, c1, p.L, sortbuf, p.norm_a[row_o], p.out_ids + (uint64_t)row_o * p.L,
+                           p.out_d + (uint64_t)row_o * p.L, lane);
+            }
+            named_bar_sync(1 + q, 64);
         }
     }
     tc_fence_before();
@@ -441,7 +495,7 @@ uint32_t cand_cap(uint32_t L) {
 
 template <int KIND, int NKA, int EPL>
 sg_status launch_t(const CUtensorMap& a, const CUtensorMap& b, KnnParams& p, cudaStream_t st) {
-    const size_t fixed = NKA * ATOM + sizeof(Bars) + 4 * 256 * 4 + 4 * 256 * 8 + 1024;
+    const size_t fixed = NKA * ATOM + sizeof(Bars) + NEPI * 256 * 4 + NEPI * 512 * 8 + 2 * BM * 4 + 1024;
     const size_t budget = 227 * 1024;
     uint32_t stages = (uint32_t)((budget - fixed) / ATOM);
     if (stages > MAX_STAGES) stages = MAX_STAGES;
@@ -475,7 +529,7 @@ sg_status launch_nka(int nka, const CUtensorMap& a, const CUtensorMap& b, KnnPar
 }  // namespace
 
 size_t knn_core_workspace(uint32_t L) {
-    return (size_t)num_sms() * BM * cand_cap(L) * sizeof(uint64_t) + 4096;
+    return (size_t)num_sms() * 2 * BM * cand_cap(L) * sizeof(uint64_t) + 4096;
 }
 
 sg_status knn_core(const Operand& A, const Operand& B, int metric, bool self_exclude, uint32_t L,
@@ -486,7 +540,7 @@ sg_status knn_core(const Operand& A, const Operand& B, int metric, bool self_exc
     p.norm_a = A.norm_a;
     p.norm_b = B.norm_b;
     p.C = cand_cap(L);
-    p.cand = cv.take<uint64_t>((size_t)num_sms() * BM * p.C);
+    p.cand = cv.take<uint64_t>((size_t)num_sms() * 2 * BM * p.C);
     if (!cv.ok()) { set_error("kNN: workspace too small"); return SG_ERR_WORKSPACE; }
     p.out_ids = ids;
     p.out_d = dists;
