@@ -84,13 +84,16 @@ sg_status cuda_status(cudaError_t e, const char* what) {
     return SG_ERR_CUDA;
 }
 
-static uint32_t knn_kdim_bytes(int prec, uint32_t d) {
-    return operand_kdim(prec, d) * (prec == SG_PREC_F16_EXACT ? 2u : 4u);
+static uint32_t knn_full_atoms(int prec, int metric, uint32_t d) {
+    uint32_t kdim, nfull, mini;
+    operand_layout(prec, metric, d, &kdim, &nfull, &mini);
+    return nfull;
 }
 
 // workspace of a kNN between ma rows and mb rows (both gathered); `same` = self-join
 static size_t knn_total_ws(uint64_t ma, uint64_t mb, uint32_t d, int prec, uint32_t L, bool same) {
-    size_t b = operand_bytes(prec, d, ma) + (same ? 0 : operand_bytes(prec, d, mb));
+    size_t b = same ? operand_bytes(prec, SG_L2, d, ma, SIDE_A | SIDE_B)
+                    : operand_bytes(prec, SG_L2, d, ma, SIDE_A) + operand_bytes(prec, SG_L2, d, mb, SIDE_B);
     return b + knn_core_workspace(L) + 4096;
 }
 
@@ -100,11 +103,11 @@ static int worst_prec(sg_dtype dtype, int32_t precision) {
     return dtype == SG_U8 ? SG_PREC_TF32 : SG_PREC_TF32;
 }
 
-static sg_status check_knn_shape(int prec, uint32_t d, uint32_t L) {
+static sg_status check_knn_shape(int prec, int metric, uint32_t d, uint32_t L) {
     SG_CHECK_ARG(L >= 1 && L <= 256, "kNN: L must be in [1, 256]");
-    const uint32_t kb = knn_kdim_bytes(prec, d);
-    if (kb > 768) {
-        set_error("kNN: d=%u needs %u operand bytes per row with this precision (max 768)", d, kb);
+    const uint32_t nf = knn_full_atoms(prec, metric, d);
+    if (nf > 6) {
+        set_error("kNN: d=%u needs %u 128-byte operand atoms per row with this precision (max 6)", d, nf);
         return SG_ERR_UNSUPPORTED;
     }
     return SG_OK;
@@ -221,12 +224,12 @@ static sg_status knn_impl(const void* xa, const uint32_t* ida, uint64_t ma, cons
     sg_status e;
     const int prec = resolve_precision(precision, dtype, d, xa, ida, ma, xb, idb, mb, flags, st, &e);
     if (e != SG_OK) return e;
-    SG_TRY(check_knn_shape(prec, d, L));
+    SG_TRY(check_knn_shape(prec, metric, d, L));
     const bool same = xa == xb && ida == idb && ma == mb;
     Operand A, B;
-    SG_TRY(gather_operand(xa, dtype, d, ida, ma, prec, metric, false, cv, &A, st));
+    SG_TRY(gather_operand(xa, dtype, d, ida, ma, prec, metric, same ? (SIDE_A | SIDE_B) : SIDE_A, cv, &A, st));
     if (same) B = A;
-    else SG_TRY(gather_operand(xb, dtype, d, idb, mb, prec, metric, true, cv, &B, st));
+    else SG_TRY(gather_operand(xb, dtype, d, idb, mb, prec, metric, SIDE_B, cv, &B, st));
     if (prec == SG_PREC_TF32X3 && !same) {
         // A side uses [hi|hi|lo]; B side uses [hi|lo|hi]: A.a and B.b are already those layouts
     }
@@ -274,7 +277,7 @@ static size_t build_ws(uint64_t m, uint32_t d, sg_dtype dtype, const sg_build_pa
     size_t b = 1024;
     b += 2 * (m * p->L * 4 + 256);     // kNN ids + dists (when not caller-provided)
     b += 2 * (m * p->R * 4 + 256);     // pruned ids + dists
-    size_t knn = operand_bytes(prec, d, m) + knn_core_workspace(p->L) + 1024;
+    size_t knn = operand_bytes(prec, p->metric, d, m, SIDE_A | SIDE_B) + knn_core_workspace(p->L) + 1024;
     size_t rev = reverse_ws(m, p->R);
     return b + (knn > rev ? knn : rev);
 }
@@ -328,11 +331,11 @@ sg_status scalegann_build_shard(const void* x, sg_dtype dtype, uint64_t n, uint3
     sg_status e;
     const int prec = resolve_precision(p->precision, dtype, d, x, idmap, m, nullptr, nullptr, 0, flags, st, &e);
     if (e != SG_OK) return e;
-    SG_TRY(check_knn_shape(prec, d, p->L));
+    SG_TRY(check_knn_shape(prec, p->metric, d, p->L));
     {
         Carver kc = cv;   // the kNN scratch is reused by the reverse stage afterwards
         Operand A;
-        SG_TRY(gather_operand(x, dtype, d, idmap, m, prec, p->metric, false, kc, &A, st));
+        SG_TRY(gather_operand(x, dtype, d, idmap, m, prec, p->metric, SIDE_A | SIDE_B, kc, &A, st));
         SG_TRY(knn_core(A, A, p->metric, true, p->L, kid, kd, nullptr, kc, st));
     }
     SG_TRY(launch_prune(kid, kd, m, p->L, p->R, p->prune_rule, pr, prd, st));

@@ -166,24 +166,32 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* tmp, u
 // (host functions implemented in the per-stage .cu files, called by api.cu)
 namespace sg {
 // gather.cu
+// Augmented tensor-core operand of a set of rows (gather.cu).  Row layout, K-major:
+//   A side (query rows i):   [a_i (or hi|hi|lo), norm multipliers, 0...]
+//   B side (column rows j):  [-2 b_j (or -b_j for IP), norm pieces of |b_j|^2, 0...]
+// so that A_i . B_j = |b_j|^2 - 2 a_i.b_j (L2) or -a_i.b_j (IP) = the selection key.
+// K = nfull 128-byte atoms + optional 32-byte mini atom.  Padding rows of the B side carry
+// +inf in the first norm column so their keys are +inf.
 struct Operand {
-    void* a = nullptr;         // rows_pad x kdim elements (f16 or f32-as-tf32)
-    void* b = nullptr;         // == a unless TF32X3
-    float* norm_a = nullptr;   // rows_pad (0 pad)
-    float* norm_b = nullptr;   // rows_pad (+inf pad for columns)
-    uint32_t kdim = 0;         // padded K in elements
+    void* a = nullptr;         // A side, rows_pad x kdim (nullptr if not built)
+    void* b = nullptr;         // B side, rows_pad x kdim (nullptr if not built)
+    float* norm = nullptr;     // rows_pad: |x|^2 (L2) or 0 (IP), for the final distance
+    uint32_t kdim = 0;         // K in elements
+    uint32_t nfull = 0;        // full 128-byte atoms
+    uint32_t mini = 0;         // 1 if a 32-byte mini atom follows
     uint32_t esize = 2;        // 2 (f16) or 4 (tf32)
     uint64_t rows = 0, rows_pad = 0;
 };
+enum { SIDE_A = 1, SIDE_B = 2 };
 // AUTO -> F16_EXACT when every referenced value is an integer with |v| <= 2048 and
 // 2*d*max^2 < 2^24 (then dots, norms and distances are exact in fp32), else TF32.
 int resolve_precision(int32_t precision, sg_dtype dtype, uint32_t d, const void* xa, const uint32_t* ida,
                       uint64_t ma, const void* xb, const uint32_t* idb, uint64_t mb, unsigned int* flags,
                       cudaStream_t st, sg_status* err);
-uint32_t operand_kdim(int prec, uint32_t d);
-size_t operand_bytes(int prec, uint32_t d, uint64_t rows);
+void operand_layout(int prec, int metric, uint32_t d, uint32_t* kdim, uint32_t* nfull, uint32_t* mini);
+size_t operand_bytes(int prec, int metric, uint32_t d, uint64_t rows, int sides);
 sg_status gather_operand(const void* x, sg_dtype dtype, uint32_t d, const uint32_t* ids, uint64_t m,
-                         int prec, int metric, bool as_columns, Carver& cv, Operand* op, cudaStream_t st);
+                         int prec, int metric, int sides, Carver& cv, Operand* op, cudaStream_t st);
 // knn_tc.cu
 size_t knn_core_workspace(uint32_t L);
 sg_status knn_core(const Operand& A, const Operand& B, int metric, bool self_exclude, uint32_t L,

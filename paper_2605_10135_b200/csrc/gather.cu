@@ -1,10 +1,15 @@
-// a4 — shard materialisation: gather rows idmap[0..m) of x into the tensor-core operand
-// layout (row-major, K padded to whole 128-byte swizzle atoms, rows padded to 128) and
-// compute the fp32 row norms used by the distance epilogue (reading R3).
-//   F16_EXACT: x -> f16 (exact for integers |v| <= 2048), K padded to 64.
-//   TF32:      x -> tf32 (cvt.rna), K padded to 32.
-//   TF32X3:    A = [hi | hi | lo], B = [hi | lo | hi] so A.B = hi.hi + hi.lo + lo.hi.
-// One warp per row; |x|^2 accumulated in fp64 and rounded once (exact for integer data).
+// a4 — shard materialisation: gather rows ids[0..m) of x into the augmented tensor-core
+// operands of the distance kernel (see Operand in common.cuh; reading R3):
+//   F16_EXACT, L2:  A = [x, 1, 2048, 2048]       B = [-2x, c0, c1, 2048 c2],
+//                   |x|^2 = c0 + 2^11 c1 + 2^22 c2 with c0, c1 < 2048 (all f16-exact), so
+//                   A_i.B_j = |b_j|^2 - 2 a_i.b_j exactly in fp32 for integer data with
+//                   2 d max^2 < 2^24 (every partial sum is an integer below 2^24).
+//   TF32, L2:       A = [tf32(x), 1, 1]          B = [-2 tf32(x), n_hi, n_lo]
+//   TF32X3, L2:     A = [hi, hi, lo, 1, 1]       B = [-2hi, -2lo, -2hi, n_hi, n_lo]
+//                   (hi = tf32(x), lo = tf32(x - hi): A.B = |b|^2 - 2(hi.hi' + hi.lo' + lo.hi'))
+//   IP:             A = [x.., 1]                 B = [-x.., 0]
+// Padding rows: A all zero; B with +inf in the first norm column (key = +inf).
+// One warp per row; |x|^2 accumulated in fp64 (exact for integer data).
 #include <cuda_fp16.h>
 
 #include "common.cuh"
@@ -19,35 +24,89 @@ __device__ __forceinline__ float to_tf32(float v) {
 }
 
 template <int PREC>
+__device__ __forceinline__ void put(void* base, uint64_t idx, float v) {
+    if constexpr (PREC == SG_PREC_F16_EXACT) ((__half*)base)[idx] = __float2half_rn(v);
+    else ((float*)base)[idx] = v;
+}
+
+template <int PREC>
 __global__ void gather_rows(const void* __restrict__ x, int dtype, uint32_t d, const uint32_t* __restrict__ ids,
-                            uint64_t m, uint64_t rows_pad, uint32_t kdim, uint32_t dpad, int metric,
+                            uint64_t m, uint64_t rows_pad, uint32_t kdim, int metric, int sides,
                             void* __restrict__ outa, void* __restrict__ outb, float* __restrict__ norm) {
     const uint64_t r = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t lane = threadIdx.x & 31;
     if (r >= rows_pad) return;
-    double s = 0.0;
     const bool real = r < m;
+    const bool l2 = metric != SG_IP;
+    const float sc = l2 ? -2.f : -1.f;
     const uint64_t src = real ? (ids ? ids[r] : r) : 0;
-    for (uint32_t j = lane; j < dpad; j += 32) {
+    const uint64_t rowA = r * kdim, rowB = r * kdim;
+    const bool doA = sides & SIDE_A, doB = sides & SIDE_B;
+    double s = 0.0;
+    const uint32_t dtot = PREC == SG_PREC_TF32X3 ? 3 * d : d;
+    for (uint32_t j = lane; j < d; j += 32) {
         float v = 0.f;
-        if (real && j < d)
-            v = dtype == SG_U8 ? (float)((const uint8_t*)x)[src * d + j] : ((const float*)x)[src * d + j];
+        if (real) v = dtype == SG_U8 ? (float)((const uint8_t*)x)[src * d + j] : ((const float*)x)[src * d + j];
         s += (double)v * (double)v;
         if constexpr (PREC == SG_PREC_F16_EXACT) {
-            ((__half*)outa)[r * kdim + j] = __float2half_rn(v);
+            if (doA) put<PREC>(outa, rowA + j, v);
+            if (doB) put<PREC>(outb, rowB + j, sc * v);
         } else if constexpr (PREC == SG_PREC_TF32) {
-            ((float*)outa)[r * kdim + j] = to_tf32(v);
+            const float t = to_tf32(v);
+            if (doA) put<PREC>(outa, rowA + j, t);
+            if (doB) put<PREC>(outb, rowB + j, sc * t);
         } else {
             const float hi = to_tf32(v), lo = to_tf32(v - hi);
-            float* A = (float*)outa + r * kdim;
-            float* B = (float*)outb + r * kdim;
-            A[j] = hi; A[dpad + j] = hi; A[2 * dpad + j] = lo;
-            B[j] = hi; B[dpad + j] = lo; B[2 * dpad + j] = hi;
+            if (doA) {
+                put<PREC>(outa, rowA + j, hi);
+                put<PREC>(outa, rowA + d + j, hi);
+                put<PREC>(outa, rowA + 2 * d + j, lo);
+            }
+            if (doB) {
+                put<PREC>(outb, rowB + j, sc * hi);
+                put<PREC>(outb, rowB + d + j, sc * lo);
+                put<PREC>(outb, rowB + 2 * d + j, sc * hi);
+            }
         }
+    }
+    const uint32_t nnorm = l2 ? (PREC == SG_PREC_F16_EXACT ? 3u : 2u) : 1u;
+    for (uint32_t j = dtot + nnorm + lane; j < kdim; j += 32) {
+        if (doA) put<PREC>(outa, rowA + j, 0.f);
+        if (doB) put<PREC>(outb, rowB + j, 0.f);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) norm[r] = real ? (metric == SG_IP ? 0.f : (float)s) : __int_as_float(0x7f800000);
+    if (lane == 0) {
+        const float INF = __int_as_float(0x7f800000);
+        if (norm) norm[r] = real && l2 ? (float)s : 0.f;
+        if (doA) {
+            if (!l2) {
+                put<PREC>(outa, rowA + dtot, real ? 1.f : 0.f);
+            } else if (PREC == SG_PREC_F16_EXACT) {
+                put<PREC>(outa, rowA + dtot, real ? 1.f : 0.f);
+                put<PREC>(outa, rowA + dtot + 1, real ? 2048.f : 0.f);
+                put<PREC>(outa, rowA + dtot + 2, real ? 2048.f : 0.f);
+            } else {
+                put<PREC>(outa, rowA + dtot, real ? 1.f : 0.f);
+                put<PREC>(outa, rowA + dtot + 1, real ? 1.f : 0.f);
+            }
+        }
+        if (doB) {
+            if (!l2) {
+                put<PREC>(outb, rowB + dtot, real ? 0.f : INF);
+            } else if (PREC == SG_PREC_F16_EXACT) {
+                const double c2 = floor(s / 4194304.0), rem = s - c2 * 4194304.0;
+                const double c1 = floor(rem / 2048.0), c0 = rem - c1 * 2048.0;
+                put<PREC>(outb, rowB + dtot, real ? (float)c0 : INF);
+                put<PREC>(outb, rowB + dtot + 1, real ? (float)c1 : 0.f);
+                put<PREC>(outb, rowB + dtot + 2, real ? (float)(2048.0 * c2) : 0.f);
+            } else {
+                const float nh = to_tf32((float)s), nl = to_tf32((float)(s - (double)nh));
+                put<PREC>(outb, rowB + dtot, real ? nh : INF);
+                put<PREC>(outb, rowB + dtot + 1, real ? nl : 0.f);
+            }
+        }
+    }
 }
 
 __global__ void exactness_probe(const float* __restrict__ x, const uint32_t* __restrict__ ids, uint64_t m,
@@ -68,18 +127,29 @@ __global__ void exactness_probe(const float* __restrict__ x, const uint32_t* __r
 
 }  // namespace
 
-uint32_t operand_kdim(int prec, uint32_t d) {
-    if (prec == SG_PREC_F16_EXACT) return (d + 63) / 64 * 64;
-    if (prec == SG_PREC_TF32) return (d + 31) / 32 * 32;
-    return 3 * ((d + 31) / 32 * 32);
+void operand_layout(int prec, int metric, uint32_t d, uint32_t* kdim, uint32_t* nfull, uint32_t* mini) {
+    const uint32_t es = prec == SG_PREC_F16_EXACT ? 2 : 4, atomk = 128 / es, minik = 32 / es;
+    const uint32_t dtot = prec == SG_PREC_TF32X3 ? 3 * d : d;
+    const uint32_t nnorm = metric == SG_IP ? 1 : (prec == SG_PREC_F16_EXACT ? 3 : 2);
+    const uint32_t ext = dtot + nnorm;
+    uint32_t nf = ext / atomk, mi = 0;
+    const uint32_t rem = ext % atomk;
+    if (rem != 0) {
+        if (rem <= minik) mi = 1;
+        else nf++;
+    }
+    *nfull = nf;
+    *mini = mi;
+    *kdim = nf * atomk + mi * minik;
 }
 
-size_t operand_bytes(int prec, uint32_t d, uint64_t rows) {
+size_t operand_bytes(int prec, int metric, uint32_t d, uint64_t rows, int sides) {
+    uint32_t kdim, nf, mi;
+    operand_layout(prec, metric, d, &kdim, &nf, &mi);
     const uint64_t rp = (rows + 127) / 128 * 128;
     const size_t e = prec == SG_PREC_F16_EXACT ? 2 : 4;
-    size_t b = rp * operand_kdim(prec, d) * e + 256;
-    if (prec == SG_PREC_TF32X3) b *= 2;
-    return b + rp * sizeof(float) + 512;
+    const int ns = ((sides & SIDE_A) ? 1 : 0) + ((sides & SIDE_B) ? 1 : 0);
+    return ns * (rp * kdim * e + 256) + rp * sizeof(float) + 1024;
 }
 
 int resolve_precision(int32_t precision, sg_dtype dtype, uint32_t d, const void* xa, const uint32_t* ida,
@@ -102,28 +172,27 @@ int resolve_precision(int32_t precision, sg_dtype dtype, uint32_t d, const void*
 }
 
 sg_status gather_operand(const void* x, sg_dtype dtype, uint32_t d, const uint32_t* ids, uint64_t m, int prec,
-                         int metric, bool /*as_columns*/, Carver& cv, Operand* op, cudaStream_t st) {
-    op->kdim = operand_kdim(prec, d);
+                         int metric, int sides, Carver& cv, Operand* op, cudaStream_t st) {
+    operand_layout(prec, metric, d, &op->kdim, &op->nfull, &op->mini);
     op->esize = prec == SG_PREC_F16_EXACT ? 2 : 4;
     op->rows = m;
     op->rows_pad = (m + 127) / 128 * 128;
     const size_t elems = op->rows_pad * op->kdim;
-    op->a = cv.take<uint8_t>(elems * op->esize);
-    op->b = prec == SG_PREC_TF32X3 ? cv.take<uint8_t>(elems * op->esize) : op->a;
-    op->norm_a = op->norm_b = cv.take<float>(op->rows_pad);
+    op->a = (sides & SIDE_A) ? cv.take<uint8_t>(elems * op->esize) : nullptr;
+    op->b = (sides & SIDE_B) ? cv.take<uint8_t>(elems * op->esize) : nullptr;
+    op->norm = cv.take<float>(op->rows_pad);
     if (!cv.ok()) { set_error("gather: workspace too small"); return SG_ERR_WORKSPACE; }
-    const uint32_t dpad = prec == SG_PREC_TF32X3 ? op->kdim / 3 : op->kdim;
     const uint64_t threads = op->rows_pad * 32;
     const unsigned grid = (unsigned)((threads + 255) / 256);
     if (prec == SG_PREC_F16_EXACT)
-        gather_rows<SG_PREC_F16_EXACT><<<grid, 256, 0, st>>>(x, dtype, d, ids, m, op->rows_pad, op->kdim, dpad, metric,
-                                                             op->a, op->b, op->norm_a);
+        gather_rows<SG_PREC_F16_EXACT><<<grid, 256, 0, st>>>(x, dtype, d, ids, m, op->rows_pad, op->kdim, metric, sides,
+                                                             op->a, op->b, op->norm);
     else if (prec == SG_PREC_TF32)
-        gather_rows<SG_PREC_TF32><<<grid, 256, 0, st>>>(x, dtype, d, ids, m, op->rows_pad, op->kdim, dpad, metric,
-                                                        op->a, op->b, op->norm_a);
+        gather_rows<SG_PREC_TF32><<<grid, 256, 0, st>>>(x, dtype, d, ids, m, op->rows_pad, op->kdim, metric, sides,
+                                                        op->a, op->b, op->norm);
     else
-        gather_rows<SG_PREC_TF32X3><<<grid, 256, 0, st>>>(x, dtype, d, ids, m, op->rows_pad, op->kdim, dpad, metric,
-                                                          op->a, op->b, op->norm_a);
+        gather_rows<SG_PREC_TF32X3><<<grid, 256, 0, st>>>(x, dtype, d, ids, m, op->rows_pad, op->kdim, metric, sides,
+                                                          op->a, op->b, op->norm);
     SG_LAUNCHED("gather_rows");
     return SG_OK;
 }

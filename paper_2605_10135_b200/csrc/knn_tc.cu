@@ -1,26 +1,30 @@
 // a5 — exact kNN: tcgen05 distance tiles + fused per-row top-L (north_star stage 2).
 //
-// dist(i, j) = |a_i|^2 + |b_j|^2 - 2 a_i.b_j (L2) or -a_i.b_j (IP) (reading R2).  The -2 a.b
-// term is a dense contraction and runs on the 5th-gen tensor cores: operands staged in
-// shared memory by TMA (128-byte swizzle), tcgen05.mma (kind::f16 or kind::tf32, fp32
-// accumulate, M=128 N=128) issued by one thread, accumulators double-buffered in TMEM and
-// read back with tcgen05.ld by four epilogue warps that fuse the top-L selection.
+// dist(i, j) = |a_i|^2 + |b_j|^2 - 2 a_i.b_j (L2) or -a_i.b_j (IP) (reading R2).  The whole
+// per-column part of the key  key(i, j) = |b_j|^2 - 2 a_i.b_j  is one dense contraction: the
+// operands are augmented (gather.cu) so that  A_i = [a_i, 1, 2048, 2048]  and
+// B_j = [-2 b_j, c0, c1, 2048 c2]  with |b_j|^2 = c0 + 2^11 c1 + 2^22 c2 (f16-exact pieces), so
+// the tensor-core accumulator IS the key (exact in fp32 for integer data: every partial sum is
+// an integer below 2^24).  dist = |a_i|^2 + key is formed once per output.
 //
-// Work decomposition (persistent, one CTA per SM):
-//   - a CTA owns 128 consecutive A rows ("row block"); its A tile stays resident in smem
-//     (NKA 16 KB swizzle atoms) while every B column tile (128 rows of B) streams through an
-//     S-stage TMA ring.  All CTAs walk the columns in the same order so the B stream is
-//     served from L2.
-//   - epilogue thread = one row (TMEM lane).  Per 32-column chunk: key = fma(scale, acc,
-//     |b_j|^2), min over the chunk, and only if min < the row's threshold are the passing
-//     (key, j) appended to the row's candidate buffer in global memory (L2 resident).
-//     Columns arrive in increasing j, so "key < threshold" realises the (dist, id) order.
-//   - when a row's buffer nears full, its warp cooperatively radix-selects the exact L
-//     smallest (key, j) pairs (8-bit digits, smem histogram) and resets the threshold to the
-//     L-th key; at the end of the row block the survivors are sorted by (dist, id).
-//
-// Warp roles (192 threads): warp 0 TMA producer, warp 1 TMEM allocator + MMA issuer,
-// warps 2..5 epilogue (warp w reads TMEM lanes 32*(w%4) .. +31).
+// Pipeline (persistent, one CTA per SM, 10 warps):
+//   warp 0: TMA producer — A row block (128 rows x K, resident in smem: NKA 128B-swizzle atoms
+//           + an optional 32B-swizzle "mini" atom holding the K tail) and the B column tiles
+//           through a ring of 16 KB slots; every CTA walks the columns in the same order so
+//           the B stream is served from L2.
+//   warp 1: TMEM allocator + single-thread tcgen05.mma issuer (kind::f16 / kind::tf32,
+//           M=128, N=128, fp32 accumulate) into a double-buffered TMEM accumulator.
+//   warps 2..9: epilogue; warp e reads TMEM lane quadrant q = warp%4 (32 rows) and column
+//           half h = e/4 (64 of the 128 columns) of every tile.  Per 32-column chunk a thread
+//           (= one row) builds a pass mask with FADD + funnel shift (sign of key - thr, 2
+//           instructions per element); only set bits are appended, as (ord(key) << 32 | col),
+//           to the row's candidate buffer (global memory, L2 resident), reading the keys back
+//           from a shared-memory stage.  Columns of a half arrive in increasing id, so the
+//           strict test realises the (dist, id) order; each half also filters with the other
+//           half's threshold (inclusive, nextup) which keeps exactness.
+//   When a buffer nears full its warp radix-selects the exact L smallest (8-bit digits,
+//   shared-memory histogram) and lowers the threshold to the L-th key.  At the end of a row
+//   block the two halves of each row are merged and sorted by (dist, id).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -29,21 +33,23 @@
 namespace sg {
 namespace {
 
-constexpr uint32_t BM = 128, BN = 128, ATOM = 128 * 128;   // bytes per swizzle atom (128 rows x 128 B)
-constexpr uint32_t NEPI = 8;                          // epilogue warps
+constexpr uint32_t BM = 128, BN = 128;
+constexpr uint32_t ATOM = 128 * 128;     // 128 rows x 128 B (128B swizzle)
+constexpr uint32_t MINIB = 128 * 32;     // 128 rows x 32 B (32B swizzle)
+constexpr uint32_t SLOT = ATOM;          // B ring slot
+constexpr uint32_t NEPI = 8;             // epilogue warps
 constexpr uint32_t NTHREADS = 64 + NEPI * 32;
-constexpr uint32_t MAX_STAGES = 12;
+constexpr uint32_t MAX_STAGES = 16;
+constexpr uint32_t KSTRIDE = 36;         // floats per staged row (16B aligned, conflict-free)
+constexpr uint32_t SCRATCH = 32 * KSTRIDE * 4;   // per epilogue warp: staged keys | hist | sort buffer
 
 // ----------------------------------------------------------------- PTX wrappers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
-                 : "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
@@ -58,20 +64,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
             "selp.u32 %0, 1, 0, p;\n\t}"
             : "=r"(ok)
             : "r"(a), "r"(parity)
-            : "memory");
-    }
-}
-// same, but lets the waiting thread sleep in hardware until the phase completes (bounded hint)
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity) {
-    uint32_t ok = 0;
-    const uint32_t a = smem_u32(b);
-    while (!ok) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(ok)
-            : "r"(a), "r"(parity), "r"(1000000u)
             : "memory");
     }
 }
@@ -105,20 +97,6 @@ __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t
             "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
     }
 }
-// tcgen05.ld 32 lanes x 32 columns of 32-bit: thread t of the warp gets row (lane base + t).
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-          "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
-          "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
-          "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-
 __device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&v)[32]) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -131,16 +109,14 @@ __device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&v)[3
         : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ uint32_t tmem_ld1(uint32_t taddr) {
-    uint32_t v;
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    return v;
-}
 
-// Shared-memory matrix descriptor: K-major, 128-byte swizzle, 8-row core groups 1024 B apart.
-__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
+// Shared-memory matrix descriptors, K-major: 128B swizzle (8-row groups 1024 B apart) and
+// 32B swizzle (8-row groups 256 B apart).
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
     return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)(1024u >> 4) << 32) | (1ull << 46) | (2ull << 61);
+}
+__device__ __forceinline__ uint64_t desc_sw32(uint32_t saddr) {
+    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)(256u >> 4) << 32) | (1ull << 46) | (6ull << 61);
 }
 
 // Instruction descriptor: D fp32, A/B f16 (KIND 0) or tf32 (KIND 1), both K-major, M=128, N=128.
@@ -149,15 +125,17 @@ __host__ __device__ constexpr uint32_t instr_desc() {
     return (1u << 4) | ((KIND ? 2u : 0u) << 7) | ((KIND ? 2u : 0u) << 10) | ((BN >> 3) << 17) | ((BM >> 4) << 24);
 }
 
+__device__ __forceinline__ float next_up(float x) {   // smallest float > x (x < +inf)
+    return x == __int_as_float(0x7f800000) ? x : ord2f(f2ord(x) + 1u);
+}
+
 struct KnnParams {
-    const float* norm_a;   // rows of A (|a|^2, or 0 for IP)
-    const float* norm_b;   // rows of B (|b|^2, or 0 for IP; +inf padding)
-    uint64_t* cand;        // gridDim.x * 128 * C candidate words
+    const float* norm_a;   // |a_i|^2 (0 for IP) for the final distance
+    uint64_t* cand;        // gridDim.x * 2 halves * 128 rows * C candidate words
     uint32_t* out_ids;     // ma x L
     float* out_d;          // ma x L
-    float* probe;          // optional raw-dot dump (ma x mb)
+    float* probe;          // optional raw accumulator dump (ma x mb)
     uint32_t ma, mb, L, C, n_rb, n_ct, stages;
-    float scale;           // -2 (L2) or -1 (IP)
     int self_exclude;
 };
 
@@ -169,14 +147,14 @@ struct __align__(8) Bars {
 };
 
 // ----------------------------------------------------------------- top-L selection
-// Warp-cooperative: keep the exactly-L smallest of row buffer rb[0..cnt) (in place at
-// rb[0..L)), return the L-th key (ordered u32).  All 32 lanes call with the same args.
+// Warp-cooperative: keep exactly the L smallest of rb[0..cnt) (in place at rb[0..L)) and
+// return the L-th key (ordered u32).  All 32 lanes call with the same arguments.
 template <int EPL>
 __device__ uint32_t select_L(uint64_t* rb, uint32_t cnt, uint32_t L, uint32_t* hist, uint32_t lane) {
     uint64_t e[EPL];
 #pragma unroll
     for (int i = 0; i < EPL; i++) {
-        uint32_t idx = i * 32 + lane;
+        const uint32_t idx = i * 32 + lane;
         e[i] = idx < cnt ? rb[idx] : ~0ull;
     }
     uint64_t pfx = 0;
@@ -190,22 +168,22 @@ __device__ uint32_t select_L(uint64_t* rb, uint32_t cnt, uint32_t L, uint32_t* h
         for (int i = 0; i < EPL; i++)
             if ((e[i] & hm) == (pfx & hm)) atomicAdd(&hist[(uint32_t)(e[i] >> sh) & 255u], 1u);
         __syncwarp();
-        uint32_t h[8], loc = 0;
+        uint32_t hv[8], loc = 0;
 #pragma unroll
-        for (int j = 0; j < 8; j++) { h[j] = hist[lane * 8 + j]; loc += h[j]; }
-        uint32_t inc = warp_incl_scan(loc, lane), exc = inc - loc;
-        bool mine = exc < want && want <= inc;
-        uint32_t bal = __ballot_sync(0xffffffffu, mine);
+        for (int j = 0; j < 8; j++) { hv[j] = hist[lane * 8 + j]; loc += hv[j]; }
+        const uint32_t inc = warp_incl_scan(loc, lane), exc = inc - loc;
+        const bool mine = exc < want && want <= inc;
+        const uint32_t bal = __ballot_sync(0xffffffffu, mine);
         uint32_t dg = 0, before = 0, bc = 0;
         if (mine) {
             uint32_t run = exc;
 #pragma unroll
             for (int j = 0; j < 8; j++) {
-                if (bc == 0 && run + h[j] >= want) { dg = lane * 8 + j; before = run; bc = h[j]; }
-                run += h[j];
+                if (bc == 0 && run + hv[j] >= want) { dg = lane * 8 + j; before = run; bc = hv[j]; }
+                run += hv[j];
             }
         }
-        int src = __ffs(bal) - 1;
+        const int src = __ffs(bal) - 1;
         dg = __shfl_sync(0xffffffffu, dg, src);
         before = __shfl_sync(0xffffffffu, before, src);
         bc = __shfl_sync(0xffffffffu, bc, src);
@@ -219,9 +197,9 @@ __device__ uint32_t select_L(uint64_t* rb, uint32_t cnt, uint32_t L, uint32_t* h
     __syncwarp();
 #pragma unroll
     for (int i = 0; i < EPL; i++) {
-        uint32_t idx = i * 32 + lane;
-        bool s = idx < cnt && (e[i] >> cut) <= lim;
-        uint32_t bal = __ballot_sync(0xffffffffu, s);
+        const uint32_t idx = i * 32 + lane;
+        const bool s = idx < cnt && (e[i] >> cut) <= lim;
+        const uint32_t bal = __ballot_sync(0xffffffffu, s);
         if (s) {
             rb[base + __popc(bal & ((1u << lane) - 1u))] = e[i];
             mk = max(mk, (uint32_t)(e[i] >> 32));
@@ -234,8 +212,8 @@ __device__ uint32_t select_L(uint64_t* rb, uint32_t cnt, uint32_t L, uint32_t* h
     return mk;
 }
 
-// Merge the two column halves' survivors of one row (each <= L, any order), sort by
-// (dist, id) with dist = |a_i|^2 + key, write the first L (sentinel / +inf padding).
+// Merge the two column halves' survivors of one row (each <= L), sort by (dist, id) with
+// dist = |a_i|^2 + key, write the first L (sentinel / +inf padding).
 __device__ void finish_row(const uint64_t* b0, uint32_t c0, const uint64_t* b1, uint32_t c1, uint32_t L,
                            uint64_t* sortbuf, float na, uint32_t* out_ids, float* out_d, uint32_t lane) {
     const uint32_t cnt = c0 + c1;
@@ -261,21 +239,25 @@ __device__ void finish_row(const uint64_t* b0, uint32_t c0, const uint64_t* b1, 
 }
 
 // ----------------------------------------------------------------- the kernel
-template <int KIND, int NKA, int EPL>
+template <int KIND, int NKA, int MINI, int EPL>
 __global__ void __launch_bounds__(NTHREADS, 1)
-knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, KnnParams p) {
+knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              const __grid_constant__ CUtensorMap tmAm, const __grid_constant__ CUtensorMap tmBm, KnnParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
+    constexpr uint32_t EL = KIND ? 4 : 2;                  // bytes per element
+    constexpr uint32_t ATOM_K = 128 / EL;                  // elements per 128B atom
+    constexpr uint32_t NSLOT = NKA + MINI;                 // ring slots per column tile
+    constexpr uint32_t A_BYTES = NKA * ATOM + (MINI ? 1024u * ((MINIB + 1023) / 1024) : 0u);
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint8_t* sA = smem;                                   // NKA atoms
-    uint8_t* sB = smem + NKA * ATOM;                      // stages atoms
-    Bars* bars = (Bars*)(sB + p.stages * ATOM);
-    uint32_t* hist_all = (uint32_t*)(bars + 1);           // NEPI x 256
-    uint64_t* sort_all = (uint64_t*)(hist_all + NEPI * 256);   // NEPI x 512
-    uint32_t* s_cnt = (uint32_t*)(sort_all + NEPI * 512);      // 2 halves x 128 rows
+    uint8_t* sA = smem;
+    uint8_t* sAm = smem + NKA * ATOM;
+    uint8_t* sB = smem + A_BYTES;
+    Bars* bars = (Bars*)(sB + p.stages * SLOT);
+    float* s_thr = (float*)(((uintptr_t)(bars + 1) + 127) & ~(uintptr_t)127);   // 2 halves x 128 rows
+    uint32_t* s_cnt = (uint32_t*)(s_thr + 2 * BM);         // 2 halves x 128 rows
+    uint8_t* scratch_all = (uint8_t*)(s_cnt + 2 * BM);     // NEPI x SCRATCH (16B aligned)
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr uint32_t EL = KIND ? 4 : 2;                 // bytes per element
-    constexpr uint32_t ATOM_K = 128 / EL;                 // elements per atom along K
 
     if (threadIdx.x == 0) {
         for (uint32_t s = 0; s < p.stages; s++) { mbar_init(&bars->full[s], 1); mbar_init(&bars->empty[s], 1); }
@@ -288,6 +270,10 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmA) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmB) : "memory");
+        if (MINI) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmAm) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmBm) : "memory");
+        }
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&bars->tmem_base)),
@@ -304,14 +290,21 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         if (lane == 0) {
             uint32_t stage = 0, sph = 0, it = 0;
             for (uint32_t rb = blockIdx.x; rb < p.n_rb; rb += gridDim.x, it++) {
-                if (it > 0) mbar_wait_sleep(&bars->a_empty, (it - 1) & 1);
-                mbar_expect_tx(&bars->a_full, NKA * ATOM);
+                if (it > 0) mbar_wait(&bars->a_empty, (it - 1) & 1);
+                mbar_expect_tx(&bars->a_full, NKA * ATOM + (MINI ? MINIB : 0u));
                 for (int ka = 0; ka < NKA; ka++) tma_load_2d(&tmA, &bars->a_full, sA + ka * ATOM, ka * ATOM_K, rb * BM);
+                if (MINI) tma_load_2d(&tmAm, &bars->a_full, sAm, NKA * ATOM_K, rb * BM);
                 for (uint32_t t = 0; t < p.n_ct; t++) {
-                    for (int ka = 0; ka < NKA; ka++) {
-                        mbar_wait_sleep(&bars->empty[stage], sph ^ 1);
-                        mbar_expect_tx(&bars->full[stage], ATOM);
-                        tma_load_2d(&tmB, &bars->full[stage], sB + stage * ATOM, ka * ATOM_K, t * BN);
+#pragma unroll
+                    for (uint32_t ka = 0; ka < NSLOT; ka++) {
+                        mbar_wait(&bars->empty[stage], sph ^ 1);
+                        if (ka < NKA) {
+                            mbar_expect_tx(&bars->full[stage], ATOM);
+                            tma_load_2d(&tmB, &bars->full[stage], sB + stage * SLOT, ka * ATOM_K, t * BN);
+                        } else {
+                            mbar_expect_tx(&bars->full[stage], MINIB);
+                            tma_load_2d(&tmBm, &bars->full[stage], sB + stage * SLOT, NKA * ATOM_K, t * BN);
+                        }
                         if (++stage == p.stages) { stage = 0; sph ^= 1; }
                     }
                 }
@@ -321,24 +314,27 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         // ===================== MMA issuer =====================
         if (lane == 0) {
             constexpr uint32_t idesc = instr_desc<KIND>();
-            const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
+            const uint32_t a_base = smem_u32(sA), am_base = smem_u32(sAm), b_base = smem_u32(sB);
             uint32_t stage = 0, sph = 0, it = 0, git = 0;
             for (uint32_t rb = blockIdx.x; rb < p.n_rb; rb += gridDim.x, it++) {
-                mbar_wait_sleep(&bars->a_full, it & 1);
+                mbar_wait(&bars->a_full, it & 1);
                 tc_fence_after();
                 for (uint32_t t = 0; t < p.n_ct; t++, git++) {
                     const uint32_t buf = git & 1;
-                    mbar_wait_sleep(&bars->tm_empty[buf], ((git >> 1) & 1) ^ 1);
+                    mbar_wait(&bars->tm_empty[buf], ((git >> 1) & 1) ^ 1);
                     tc_fence_after();
                     const uint32_t dcol = tmem + buf * BN;
-                    for (int ka = 0; ka < NKA; ka++) {
-                        mbar_wait_sleep(&bars->full[stage], sph);
-                        tc_fence_after();
 #pragma unroll
-                        for (uint32_t kk = 0; kk < 4; kk++) {
-                            uint64_t ad = smem_desc(a_base + ka * ATOM + kk * 32);
-                            uint64_t bd = smem_desc(b_base + stage * ATOM + kk * 32);
-                            tc_mma<KIND>(dcol, ad, bd, idesc, (ka | kk) != 0);
+                    for (uint32_t ka = 0; ka < NSLOT; ka++) {
+                        mbar_wait(&bars->full[stage], sph);
+                        tc_fence_after();
+                        if (ka < NKA) {
+#pragma unroll
+                            for (uint32_t kk = 0; kk < 4; kk++)
+                                tc_mma<KIND>(dcol, desc_sw128(a_base + ka * ATOM + kk * 32),
+                                             desc_sw128(b_base + stage * SLOT + kk * 32), idesc, (ka | kk) != 0);
+                        } else {
+                            tc_mma<KIND>(dcol, desc_sw32(am_base), desc_sw32(b_base + stage * SLOT), idesc, NKA != 0);
                         }
                         tc_commit(&bars->empty[stage]);
                         if (++stage == p.stages) { stage = 0; sph ^= 1; }
@@ -349,12 +345,13 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             }
         }
     } else {
-        // ===================== epilogue: fused distance + top-L =====================
-        // warp e = warp-2 in 0..7: TMEM lane quadrant q (rows q*32..), column half h (64 cols)
+        // ===================== epilogue: fused selection =====================
         const uint32_t e = warp - 2, q = warp & 3, h = e >> 2;
-        const uint32_t r = q * 32 + lane;                   // row within the block
-        uint32_t* hist = hist_all + e * 256;
-        uint64_t* sortbuf = sort_all + e * 512;
+        const uint32_t r = q * 32 + lane;                    // row within the block
+        uint8_t* scratch = scratch_all + e * SCRATCH;
+        float* skeys = (float*)scratch;                      // [32][KSTRIDE] staged keys
+        uint32_t* hist = (uint32_t*)scratch;                 // 256 (aliases skeys)
+        uint64_t* sortbuf = (uint64_t*)scratch;              // 512 (aliases skeys)
         const uint32_t C = p.C;
         uint64_t* half_base = p.cand + ((uint64_t)blockIdx.x * 2 + h) * BM * C;
         uint64_t* myrow = half_base + (uint64_t)r * C;
@@ -367,15 +364,20 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             const bool valid = row < p.ma;
             float thr = valid ? INF : -INF;
             uint32_t cnt = 0;
+            s_thr[h * BM + r] = thr;
+            named_bar_sync(1 + q, 64);
             for (uint32_t t = 0; t < p.n_ct; t++, git++) {
                 const uint32_t buf = git & 1;
-                mbar_wait_sleep(&bars->tm_full[buf], (git >> 1) & 1);
+                mbar_wait(&bars->tm_full[buf], (git >> 1) & 1);
                 tc_fence_after();
                 const uint32_t tb = tl + buf * BN;
                 uint32_t v[2][32];
                 tmem_ld32_nowait(tb, v[0]);
                 tmem_ld32_nowait(tb + 32, v[1]);
                 tmem_wait_ld();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->tm_empty[buf]);   // accumulator now in registers
                 const bool diag = p.self_exclude && t == rb;
 #pragma unroll
                 for (uint32_t ch = 0; ch < 2; ch++) {
@@ -392,41 +394,37 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                         const int o = __ffs(need) - 1;
                         need &= need - 1;
                         const uint32_t c_o = __shfl_sync(0xffffffffu, cnt, o);
-                        uint32_t kth = select_L<EPL>(warprows + (uint64_t)o * C, c_o, p.L, hist, lane);
-                        if (lane == (uint32_t)o) { cnt = p.L; thr = ord2f(kth); }
-                    }
-                    const float4* nb4 = (const float4*)(p.norm_b + col0);
-                    uint32_t mask = 0;
-#pragma unroll
-                    for (int j4 = 0; j4 < 8; j4++) {
-                        const float4 nb = __ldg(nb4 + j4);
-                        const float k0 = fmaf(p.scale, __uint_as_float(v[ch][4 * j4 + 0]), nb.x);
-                        const float k1 = fmaf(p.scale, __uint_as_float(v[ch][4 * j4 + 1]), nb.y);
-                        const float k2 = fmaf(p.scale, __uint_as_float(v[ch][4 * j4 + 2]), nb.z);
-                        const float k3 = fmaf(p.scale, __uint_as_float(v[ch][4 * j4 + 3]), nb.w);
-                        mask |= (k0 < thr ? 1u : 0u) << (4 * j4 + 0);
-                        mask |= (k1 < thr ? 1u : 0u) << (4 * j4 + 1);
-                        mask |= (k2 < thr ? 1u : 0u) << (4 * j4 + 2);
-                        mask |= (k3 < thr ? 1u : 0u) << (4 * j4 + 3);
-                    }
-                    if (diag && ch + 2 * h == q) mask &= ~(1u << lane);   // self column
-                    // rare path: walk the union of passing columns (warp-uniform), re-read each
-                    // column from TMEM (uniform address) and append where this row passes
-                    uint32_t U = __reduce_or_sync(0xffffffffu, mask);
-                    while (U) {
-                        const uint32_t c = __ffs(U) - 1;
-                        U &= U - 1;
-                        const uint32_t raw = tmem_ld1(tb + ch * 32 + c);
-                        if ((mask >> c) & 1u) {
-                            const float kv = fmaf(p.scale, __uint_as_float(raw), __ldg(p.norm_b + col0 + c));
-                            myrow[cnt] = ((uint64_t)f2ord(kv) << 32) | (col0 + c);
-                            cnt++;
+                        const uint32_t kth = select_L<EPL>(warprows + (uint64_t)o * C, c_o, p.L, hist, lane);
+                        if (lane == (uint32_t)o) {
+                            cnt = p.L;
+                            thr = ord2f(kth);
+                            s_thr[h * BM + r] = thr;
                         }
                     }
+                    const float te = fminf(thr, next_up(s_thr[(h ^ 1) * BM + r]));
+                    // pass mask: bit j = sign(key_j - te)  (key < te; NaN / equal -> 0)
+                    uint32_t mask = 0;
+#pragma unroll
+                    for (int j = 31; j >= 0; j--)
+                        mask = __funnelshift_l(__float_as_uint(__fsub_rn(__uint_as_float(v[ch][j]), te)), mask, 1);
+                    if (diag && ch + 2 * h == q) mask &= ~(1u << lane);   // self column
+                    if (__any_sync(0xffffffffu, mask != 0)) {
+                        float4* mine = (float4*)(skeys + lane * KSTRIDE);
+#pragma unroll
+                        for (int j4 = 0; j4 < 8; j4++)
+                            mine[j4] = make_float4(__uint_as_float(v[ch][4 * j4]), __uint_as_float(v[ch][4 * j4 + 1]),
+                                                   __uint_as_float(v[ch][4 * j4 + 2]),
+                                                   __uint_as_float(v[ch][4 * j4 + 3]));
+                        __syncwarp();
+                        while (mask) {
+                            const uint32_t c = __ffs(mask) - 1;
+                            mask &= mask - 1;
+                            const float kv = skeys[lane * KSTRIDE + c];
+                            myrow[cnt++] = ((uint64_t)f2ord(kv) << 32) | (col0 + c);
+                        }
+                        __syncwarp();
+                    }
                 }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&bars->tm_empty[buf]);
             }
             if (p.probe) continue;
             // ---- final: each half keeps its exact top-L, then the two halves of a row are merged
@@ -442,11 +440,10 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 const uint32_t rr = q * 32 + h * 16 + i;
                 const uint32_t row_o = rb * BM + rr;
                 if (row_o >= p.ma) continue;
-                const uint32_t c0 = s_cnt[rr], c1 = s_cnt[BM + rr];
                 const uint64_t* b0 = p.cand + ((uint64_t)blockIdx.x * 2 + 0) * BM * C + (uint64_t)rr * C;
                 const uint64_t* b1 = p.cand + ((uint64_t)blockIdx.x * 2 + 1) * BM * C + (uint64_t)rr * C;
-                finish_row(b0, c0, b1, c1, p.L, sortbuf, p.norm_a[row_o], p.out_ids + (uint64_t)row_o * p.L,
-                           p.out_d + (uint64_t)row_o * p.L, lane);
+                finish_row(b0, s_cnt[rr], b1, s_cnt[BM + rr], p.L, sortbuf, p.norm_a[row_o],
+                           p.out_ids + (uint64_t)row_o * p.L, p.out_d + (uint64_t)row_o * p.L, lane);
             }
             named_bar_sync(1 + q, 64);
         }
@@ -463,26 +460,27 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     if (!fn) {
-        cudaDriverEntryPointQueryResult q;
+        cudaDriverEntryPointQueryResult qr;
         void* ptr = nullptr;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &qr) == cudaSuccess &&
+            qr == cudaDriverEntryPointSuccess)
             fn = (PFN_cuTensorMapEncodeTiled_v12000)ptr;
     }
     return fn;
 }
 
-sg_status make_map(CUtensorMap* m, const void* base, uint64_t rows, uint32_t kdim, uint32_t esize) {
+// 2-D map over a rows x kdim operand; box = (box_bytes / esize) elements x 128 rows.
+sg_status make_map(CUtensorMap* m, const void* base, uint64_t rows, uint32_t kdim, uint32_t esize, uint32_t box_bytes) {
     auto enc = get_encode();
     if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return SG_ERR_CUDA; }
     cuuint64_t dims[2] = {kdim, rows};
     cuuint64_t strides[1] = {(cuuint64_t)kdim * esize};
-    cuuint32_t box[2] = {128u / esize, 128u};
+    cuuint32_t box[2] = {box_bytes / esize, 128u};
     cuuint32_t es[2] = {1, 1};
+    const CUtensorMapSwizzle sw = box_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B;
     CUresult r = enc(m, esize == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
-                     const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                     const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) { set_error("cuTensorMapEncodeTiled failed (%d)", (int)r); return SG_ERR_CUDA; }
     return SG_OK;
 }
@@ -493,37 +491,43 @@ uint32_t cand_cap(uint32_t L) {
     return c;
 }
 
-template <int KIND, int NKA, int EPL>
-sg_status launch_t(const CUtensorMap& a, const CUtensorMap& b, KnnParams& p, cudaStream_t st) {
-    const size_t fixed = NKA * ATOM + sizeof(Bars) + NEPI * 256 * 4 + NEPI * 512 * 8 + 2 * BM * 4 + 1024;
+template <int KIND, int NKA, int MINI, int EPL>
+sg_status launch_t(const CUtensorMap* maps, KnnParams& p, cudaStream_t st) {
+    constexpr uint32_t A_BYTES = NKA * ATOM + (MINI ? 1024u * ((MINIB + 1023) / 1024) : 0u);
+    const size_t fixed = A_BYTES + sizeof(Bars) + 128 + 4 * BM * 4 + NEPI * SCRATCH + 1024 + 64;
     const size_t budget = 227 * 1024;
-    uint32_t stages = (uint32_t)((budget - fixed) / ATOM);
+    uint32_t stages = (uint32_t)((budget - fixed) / SLOT);
     if (stages > MAX_STAGES) stages = MAX_STAGES;
-    if (stages < 2) { set_error("kNN: operand too wide for shared memory"); return SG_ERR_UNSUPPORTED; }
+    if (stages < NKA + MINI) { set_error("kNN: operand too wide for shared memory"); return SG_ERR_UNSUPPORTED; }
     p.stages = stages;
-    const size_t smem = fixed + stages * ATOM;
-    auto kern = knn_tc_kernel<KIND, NKA, EPL>;
+    const size_t smem = fixed + stages * SLOT;
+    auto kern = knn_tc_kernel<KIND, NKA, MINI, EPL>;
     SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const uint32_t grid = p.n_rb < (uint32_t)num_sms() ? p.n_rb : (uint32_t)num_sms();
     knn_time_begin(st);
-    kern<<<grid, NTHREADS, smem, st>>>(a, b, p);
+    kern<<<grid, NTHREADS, smem, st>>>(maps[0], maps[1], maps[2], maps[3], p);
     SG_LAUNCHED("knn_tc_kernel");
     knn_time_end(st);
     return SG_OK;
 }
 
-template <int KIND, int EPL>
-sg_status launch_nka(int nka, const CUtensorMap& a, const CUtensorMap& b, KnnParams& p, cudaStream_t st) {
+template <int KIND, int MINI, int EPL>
+sg_status launch_nka(int nka, const CUtensorMap* maps, KnnParams& p, cudaStream_t st) {
     switch (nka) {
-        case 1: return launch_t<KIND, 1, EPL>(a, b, p, st);
-        case 2: return launch_t<KIND, 2, EPL>(a, b, p, st);
-        case 3: return launch_t<KIND, 3, EPL>(a, b, p, st);
-        case 4: return launch_t<KIND, 4, EPL>(a, b, p, st);
-        case 5: return launch_t<KIND, 5, EPL>(a, b, p, st);
-        case 6: return launch_t<KIND, 6, EPL>(a, b, p, st);
+        case 1: return launch_t<KIND, 1, MINI, EPL>(maps, p, st);
+        case 2: return launch_t<KIND, 2, MINI, EPL>(maps, p, st);
+        case 3: return launch_t<KIND, 3, MINI, EPL>(maps, p, st);
+        case 4: return launch_t<KIND, 4, MINI, EPL>(maps, p, st);
+        case 5: return launch_t<KIND, 5, MINI, EPL>(maps, p, st);
+        case 6: return launch_t<KIND, 6, MINI, EPL>(maps, p, st);
     }
     set_error("kNN: unsupported operand width (%d atoms)", nka);
     return SG_ERR_UNSUPPORTED;
+}
+
+template <int KIND, int EPL>
+sg_status launch_mini(int nka, int mini, const CUtensorMap* maps, KnnParams& p, cudaStream_t st) {
+    return mini ? launch_nka<KIND, 1, EPL>(nka, maps, p, st) : launch_nka<KIND, 0, EPL>(nka, maps, p, st);
 }
 
 }  // namespace
@@ -532,13 +536,14 @@ size_t knn_core_workspace(uint32_t L) {
     return (size_t)num_sms() * 2 * BM * cand_cap(L) * sizeof(uint64_t) + 4096;
 }
 
-sg_status knn_core(const Operand& A, const Operand& B, int metric, bool self_exclude, uint32_t L,
-                   uint32_t* ids, float* dists, float* probe, Carver& cv, cudaStream_t st) {
-    if (A.kdim != B.kdim || A.esize != B.esize) { set_error("kNN: operand mismatch"); return SG_ERR_INVALID_ARG; }
-    const int nka = (int)(A.kdim * A.esize / 128);
+sg_status knn_core(const Operand& A, const Operand& B, int /*metric*/, bool self_exclude, uint32_t L, uint32_t* ids,
+                   float* dists, float* probe, Carver& cv, cudaStream_t st) {
+    if (A.kdim != B.kdim || A.esize != B.esize || A.nfull != B.nfull || A.mini != B.mini) {
+        set_error("kNN: operand layout mismatch");
+        return SG_ERR_INVALID_ARG;
+    }
     KnnParams p{};
-    p.norm_a = A.norm_a;
-    p.norm_b = B.norm_b;
+    p.norm_a = A.norm;
     p.C = cand_cap(L);
     p.cand = cv.take<uint64_t>((size_t)num_sms() * 2 * BM * p.C);
     if (!cv.ok()) { set_error("kNN: workspace too small"); return SG_ERR_WORKSPACE; }
@@ -550,21 +555,27 @@ sg_status knn_core(const Operand& A, const Operand& B, int metric, bool self_exc
     p.L = L;
     p.n_rb = (uint32_t)(A.rows_pad / BM);
     p.n_ct = (uint32_t)(B.rows_pad / BN);
-    p.scale = metric == SG_IP ? -1.f : -2.f;
     p.self_exclude = self_exclude ? 1 : 0;
-    CUtensorMap ma, mb;
-    SG_TRY(make_map(&ma, A.a, A.rows_pad, A.kdim, A.esize));
-    SG_TRY(make_map(&mb, B.b, B.rows_pad, B.kdim, B.esize));
-    const bool tf32 = A.esize == 4;
-    const int epl = (int)(p.C / 32);
-    if (tf32) {
-        if (epl <= 4) return launch_nka<1, 4>(nka, ma, mb, p, st);
-        if (epl <= 16) return launch_nka<1, 16>(nka, ma, mb, p, st);
-        return launch_nka<1, 32>(nka, ma, mb, p, st);
+    CUtensorMap maps[4];
+    SG_TRY(make_map(&maps[0], A.a, A.rows_pad, A.kdim, A.esize, 128));
+    SG_TRY(make_map(&maps[1], B.b, B.rows_pad, B.kdim, B.esize, 128));
+    if (A.mini) {
+        SG_TRY(make_map(&maps[2], A.a, A.rows_pad, A.kdim, A.esize, 32));
+        SG_TRY(make_map(&maps[3], B.b, B.rows_pad, B.kdim, B.esize, 32));
+    } else {
+        maps[2] = maps[0];
+        maps[3] = maps[1];
     }
-    if (epl <= 4) return launch_nka<0, 4>(nka, ma, mb, p, st);
-    if (epl <= 16) return launch_nka<0, 16>(nka, ma, mb, p, st);
-    return launch_nka<0, 32>(nka, ma, mb, p, st);
+    const int epl = (int)(p.C / 32);
+    const int nka = (int)A.nfull, mini = (int)A.mini;
+    if (A.esize == 4) {
+        if (epl <= 4) return launch_mini<1, 4>(nka, mini, maps, p, st);
+        if (epl <= 16) return launch_mini<1, 16>(nka, mini, maps, p, st);
+        return launch_mini<1, 32>(nka, mini, maps, p, st);
+    }
+    if (epl <= 4) return launch_mini<0, 4>(nka, mini, maps, p, st);
+    if (epl <= 16) return launch_mini<0, 16>(nka, mini, maps, p, st);
+    return launch_mini<0, 32>(nka, mini, maps, p, st);
 }
 
 }  // namespace sg

@@ -38,12 +38,13 @@ def test_gemm_probe_matches_matmul(api, prec):
     xb = datagen.sift_like(260, 128, seed=2)
     if prec == 2:
         xa, xb = datagen.gaussian(300, 128, seed=1), datagen.gaussian(260, 128, seed=2)
+    # the augmented operands make the accumulator the selection key |b_j|^2 - 2 a_i.b_j
     out = api.scalegann_gemm_probe(xa.cuda(), xb.cuda(), precision=prec).cpu()
-    ref = xa.double() @ xb.double().T
+    ref = (xb.double() ** 2).sum(1)[None, :] - 2 * (xa.double() @ xb.double().T)
     if prec == 1:   # integer data on kind::f16 with fp32 accumulation: exact
         assert torch.equal(out.double(), ref)
     else:
-        assert torch.allclose(out.double(), ref, rtol=0, atol=2e-2 * ref.abs().max().item() ** 0.5)
+        assert torch.allclose(out.double(), ref, rtol=0, atol=5e-2 * ref.abs().max().item() ** 0.5)
 
 
 # ------------------------------------------------------------------ a5 kNN
