@@ -125,6 +125,17 @@ __host__ __device__ constexpr uint32_t instr_desc() {
     return (1u << 4) | ((KIND ? 2u : 0u) << 7) | ((KIND ? 2u : 0u) << 10) | ((BN >> 3) << 17) | ((BM >> 4) << 24);
 }
 
+// (a - t, b - t) with one packed FADD2 (sm_100); results as raw bits
+__device__ __forceinline__ void sub2(uint32_t a, uint32_t b, float t, uint32_t& ra, uint32_t& rb) {
+    asm("{\n\t.reg .b64 x, y, z;\n\t"
+        "mov.b64 x, {%2, %3};\n\t"
+        "mov.b64 y, {%4, %4};\n\t"
+        "sub.rn.f32x2 z, x, y;\n\t"
+        "mov.b64 {%0, %1}, z;\n\t}"
+        : "=r"(ra), "=r"(rb)
+        : "r"(a), "r"(b), "r"(__float_as_uint(t)));
+}
+
 __device__ __forceinline__ float next_up(float x) {   // smallest float > x (x < +inf)
     return x == __int_as_float(0x7f800000) ? x : ord2f(f2ord(x) + 1u);
 }
@@ -149,13 +160,22 @@ struct __align__(8) Bars {
 // ----------------------------------------------------------------- top-L selection
 // Warp-cooperative: keep exactly the L smallest of rb[0..cnt) (in place at rb[0..L)) and
 // return the L-th key (ordered u32).  All 32 lanes call with the same arguments.
+// Candidate words are stored raw as (float bits << 32 | col); selection works on the ordered
+// form (ord(key) << 32 | col) whose unsigned order is the (key, col) order.
+__device__ __forceinline__ uint64_t raw2ord(uint64_t w) {
+    return ((uint64_t)f2ord(__uint_as_float((uint32_t)(w >> 32))) << 32) | (uint32_t)w;
+}
+__device__ __forceinline__ uint64_t ord2raw(uint64_t w) {
+    return ((uint64_t)__float_as_uint(ord2f((uint32_t)(w >> 32))) << 32) | (uint32_t)w;
+}
+
 template <int EPL>
 __device__ uint32_t select_L(uint64_t* rb, uint32_t cnt, uint32_t L, uint32_t* hist, uint32_t lane) {
     uint64_t e[EPL];
 #pragma unroll
     for (int i = 0; i < EPL; i++) {
         const uint32_t idx = i * 32 + lane;
-        e[i] = idx < cnt ? rb[idx] : ~0ull;
+        e[i] = idx < cnt ? raw2ord(rb[idx]) : ~0ull;
     }
     uint64_t pfx = 0;
     uint32_t want = L, cut = 0;
@@ -201,7 +221,7 @@ __device__ uint32_t select_L(uint64_t* rb, uint32_t cnt, uint32_t L, uint32_t* h
         const bool s = idx < cnt && (e[i] >> cut) <= lim;
         const uint32_t bal = __ballot_sync(0xffffffffu, s);
         if (s) {
-            rb[base + __popc(bal & ((1u << lane) - 1u))] = e[i];
+            rb[base + __popc(bal & ((1u << lane) - 1u))] = ord2raw(e[i]);
             mk = max(mk, (uint32_t)(e[i] >> 32));
         }
         base += __popc(bal);
@@ -223,7 +243,7 @@ __device__ void finish_row(const uint64_t* b0, uint32_t c0, const uint64_t* b1, 
         uint64_t w = ~0ull;
         if (p < cnt) {
             const uint64_t e = p < c0 ? b0[p] : b1[p - c0];
-            const float dist = na + ord2f((uint32_t)(e >> 32));
+            const float dist = na + __uint_as_float((uint32_t)(e >> 32));
             w = ((uint64_t)f2ord(dist) << 32) | (uint32_t)e;
         }
         sortbuf[p] = w;
@@ -378,37 +398,50 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->tm_empty[buf]);   // accumulator now in registers
-                const bool diag = p.self_exclude && t == rb;
-#pragma unroll
-                for (uint32_t ch = 0; ch < 2; ch++) {
-                    const uint32_t col0 = t * BN + h * 64 + ch * 32;
-                    if (p.probe) {
-                        if (valid)
+                const uint32_t colh = t * BN + h * 64;
+                if (p.probe) {
+                    if (valid)
+                        for (int ch = 0; ch < 2; ch++)
                             for (int j = 0; j < 32; j++)
-                                if (col0 + j < p.mb) p.probe[(uint64_t)row * p.mb + col0 + j] = __uint_as_float(v[ch][j]);
-                        continue;
+                                if (colh + ch * 32 + j < p.mb)
+                                    p.probe[(uint64_t)row * p.mb + colh + ch * 32 + j] = __uint_as_float(v[ch][j]);
+                    continue;
+                }
+                // make room: rows whose buffer cannot take another 64 candidates are compacted
+                uint32_t need = __ballot_sync(0xffffffffu, cnt > C - 64);
+                while (need) {
+                    const int o = __ffs(need) - 1;
+                    need &= need - 1;
+                    const uint32_t c_o = __shfl_sync(0xffffffffu, cnt, o);
+                    const uint32_t kth = select_L<EPL>(warprows + (uint64_t)o * C, c_o, p.L, hist, lane);
+                    if (lane == (uint32_t)o) {
+                        cnt = p.L;
+                        thr = ord2f(kth);
+                        s_thr[h * BM + r] = thr;
                     }
-                    // make room: rows whose buffer cannot take another 32 candidates are compacted
-                    uint32_t need = __ballot_sync(0xffffffffu, cnt > C - 32);
-                    while (need) {
-                        const int o = __ffs(need) - 1;
-                        need &= need - 1;
-                        const uint32_t c_o = __shfl_sync(0xffffffffu, cnt, o);
-                        const uint32_t kth = select_L<EPL>(warprows + (uint64_t)o * C, c_o, p.L, hist, lane);
-                        if (lane == (uint32_t)o) {
-                            cnt = p.L;
-                            thr = ord2f(kth);
-                            s_thr[h * BM + r] = thr;
-                        }
-                    }
-                    const float te = fminf(thr, next_up(s_thr[(h ^ 1) * BM + r]));
-                    // pass mask: bit j = sign(key_j - te)  (key < te; NaN / equal -> 0)
-                    uint32_t mask = 0;
+                }
+                const float te = fminf(thr, next_up(s_thr[(h ^ 1) * BM + r]));
+                // pass masks: bit j = sign(key_j - te)  (key < te; NaN / equal -> 0), two
+                // subtractions per FADD2, one funnel shift per element
+                uint32_t mk[2];
 #pragma unroll
-                    for (int j = 31; j >= 0; j--)
-                        mask = __funnelshift_l(__float_as_uint(__fsub_rn(__uint_as_float(v[ch][j]), te)), mask, 1);
-                    if (diag && ch + 2 * h == q) mask &= ~(1u << lane);   // self column
-                    if (__any_sync(0xffffffffu, mask != 0)) {
+                for (int ch = 0; ch < 2; ch++) {
+                    uint32_t m = 0;
+#pragma unroll
+                    for (int j = 31; j >= 1; j -= 2) {
+                        uint32_t lo, hi;
+                        sub2(v[ch][j - 1], v[ch][j], te, lo, hi);
+                        m = __funnelshift_l(hi, m, 1);
+                        m = __funnelshift_l(lo, m, 1);
+                    }
+                    mk[ch] = m;
+                }
+                if (p.self_exclude && t == rb && (q >> 1) == h) mk[q & 1] &= ~(1u << lane);   // self column
+                if (__any_sync(0xffffffffu, (mk[0] | mk[1]) != 0)) {
+#pragma unroll
+                    for (int ch = 0; ch < 2; ch++) {
+                        uint32_t m = mk[ch];
+                        if (!__any_sync(0xffffffffu, m != 0)) continue;
                         float4* mine = (float4*)(skeys + lane * KSTRIDE);
 #pragma unroll
                         for (int j4 = 0; j4 < 8; j4++)
@@ -416,11 +449,12 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                                                    __uint_as_float(v[ch][4 * j4 + 2]),
                                                    __uint_as_float(v[ch][4 * j4 + 3]));
                         __syncwarp();
-                        while (mask) {
-                            const uint32_t c = __ffs(mask) - 1;
-                            mask &= mask - 1;
-                            const float kv = skeys[lane * KSTRIDE + c];
-                            myrow[cnt++] = ((uint64_t)f2ord(kv) << 32) | (col0 + c);
+                        const uint32_t cb = colh + ch * 32;
+                        while (m) {
+                            const uint32_t c = 31 - __clz(m);
+                            m ^= 1u << c;
+                            const uint32_t kb = __float_as_uint(skeys[lane * KSTRIDE + c]);
+                            myrow[cnt++] = ((uint64_t)kb << 32) | (cb + c);
                         }
                         __syncwarp();
                     }
