@@ -243,6 +243,11 @@ sg_status scalegann_gemm_probe(const void* xa, uint64_t ma, const void* xb, uint
  * the summed device time, the number of distance launches and of all launches since the last
  * reset. */
 sg_status scalegann_stats_enable(int on);
+/* Diagnostics: when dev_counters (device, 80 x uint64, zeroed by the caller) is not NULL, every
+ * later distance-kernel launch adds per-warp clock64 cycle counts to it: [warp*8 + i] with
+ * i = 0 barrier waits, 1 TMEM load / full-barrier wait, 2 compaction, 3 pass masks,
+ * 4 insertions, 5 final merge.  NULL disables. */
+sg_status scalegann_knn_profile(unsigned long long* dev_counters);
 sg_status scalegann_stats_read(double* knn_ms, uint64_t* knn_launches, uint64_t* kernel_launches, int reset);
 
 #ifdef __cplusplus

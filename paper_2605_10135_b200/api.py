@@ -47,7 +47,7 @@ EXPORTS = [
     "scalegann_prune", "scalegann_reverse_workspace", "scalegann_reverse", "scalegann_build_shard_workspace",
     "scalegann_build_shard", "scalegann_optimize_from_knn", "scalegann_merge_counts", "scalegann_merge_workspace",
     "scalegann_merge_pack", "scalegann_merge_union", "scalegann_merge", "scalegann_search_workspace",
-    "scalegann_search_eval", "scalegann_gemm_probe", "scalegann_stats_enable", "scalegann_stats_read",
+    "scalegann_search_eval", "scalegann_gemm_probe", "scalegann_stats_enable", "scalegann_stats_read", "scalegann_knn_profile",
 ]
 
 
@@ -102,6 +102,7 @@ def load(build_if_missing: bool = True):
                                    P(ctypes.c_double), vp, sz, vp], i32),
         "scalegann_gemm_probe": ([vp, u64, vp, u64, i32, u32, i32, vp, vp, sz, vp], i32),
         "scalegann_stats_enable": ([ctypes.c_int], i32),
+        "scalegann_knn_profile": ([vp], i32),
         "scalegann_stats_read": ([P(ctypes.c_double), pu64, pu64, ctypes.c_int], i32),
     }
     for name, (args, res) in sig.items():
@@ -405,6 +406,11 @@ def scalegann_stats_read(reset=True):
     al = ctypes.c_uint64(0)
     _check(load().scalegann_stats_read(ctypes.byref(ms), ctypes.byref(kl), ctypes.byref(al), int(reset)))
     return ms.value, kl.value, al.value
+
+
+def scalegann_knn_profile(counters=None):
+    """Attach (or detach with None) an 80-entry int64 CUDA tensor of per-warp cycle counters."""
+    _check(load().scalegann_knn_profile(_ptr(counters)))
 
 
 # ----------------------------------------------------------------------------- a9

@@ -43,6 +43,7 @@ sg_status beam_run(const void* x, sg_dtype dtype, uint64_t n, uint32_t d, const 
 sg_status recall_run(const uint32_t* ret, const uint32_t* gt, uint32_t nq, uint32_t topk, double* recall_host,
                      Carver& cv, cudaStream_t st);
 
+void set_knn_profile(unsigned long long* buf);
 static thread_local char g_err[512] = "";
 
 // ---- diagnostics: launch counter + event timing of the distance kernel
@@ -94,7 +95,7 @@ static uint32_t knn_full_atoms(int prec, int metric, uint32_t d) {
 static size_t knn_total_ws(uint64_t ma, uint64_t mb, uint32_t d, int prec, uint32_t L, bool same) {
     size_t b = same ? operand_bytes(prec, SG_L2, d, ma, SIDE_A | SIDE_B)
                     : operand_bytes(prec, SG_L2, d, ma, SIDE_A) + operand_bytes(prec, SG_L2, d, mb, SIDE_B);
-    return b + knn_core_workspace(L) + 4096;
+    return b + knn_core_workspace(L) + 2 * (ma * 4 + 256) + (same ? order_workspace(ma, d, prec, SG_L2) : 0) + 4096;
 }
 
 static int worst_prec(sg_dtype dtype, int32_t precision) {
@@ -121,6 +122,11 @@ extern "C" {
 
 int scalegann_abi_version(void) { return SCALEGANN_ABI_VERSION; }
 const char* scalegann_last_error(void) { return g_err; }
+
+sg_status scalegann_knn_profile(unsigned long long* dev_counters) {
+    set_knn_profile(dev_counters);
+    return SG_OK;
+}
 
 sg_status scalegann_stats_enable(int on) {
     g_stats.on = on != 0;
@@ -205,7 +211,8 @@ sg_status scalegann_entry_points(const uint32_t* home, const float* primary_d, u
 sg_status scalegann_knn_workspace(uint64_t ma, uint64_t mb, uint32_t d, sg_dtype dtype, uint32_t L, int32_t precision,
                                   size_t* bytes) {
     SG_CHECK_ARG(bytes, "null bytes");
-    *bytes = knn_total_ws(ma, mb, d, worst_prec(dtype, precision), L, false);
+    const int pr = worst_prec(dtype, precision);
+    *bytes = knn_total_ws(ma, mb, d, pr, L, false) + (ma == mb ? order_workspace(ma, d, pr, SG_L2) : 0);
     return SG_OK;
 }
 
@@ -227,6 +234,15 @@ static sg_status knn_impl(const void* xa, const uint32_t* ida, uint64_t ma, cons
     SG_TRY(check_knn_shape(prec, metric, d, L));
     const bool same = xa == xb && ida == idb && ma == mb;
     Operand A, B;
+    if (same && self_exclude && !probe && order_groups(ma) >= 2) {
+        // self-join: spatially ordered operand (order.cu), results mapped back to input order
+        uint32_t* perm = cv.take<uint32_t>(ma);
+        uint32_t* ids_perm = cv.take<uint32_t>(ma);
+        if (!cv.ok()) { set_error("kNN: workspace too small"); return SG_ERR_WORKSPACE; }
+        SG_TRY(spatial_order(xa, dtype, d, ida, ma, prec, metric, perm, ids_perm, cv, st));
+        SG_TRY(gather_operand(xa, dtype, d, ids_perm, ma, prec, metric, SIDE_A | SIDE_B, cv, &A, st));
+        return knn_core(A, A, metric, true, L, ids, dists, nullptr, cv, st, perm, perm, true);
+    }
     SG_TRY(gather_operand(xa, dtype, d, ida, ma, prec, metric, same ? (SIDE_A | SIDE_B) : SIDE_A, cv, &A, st));
     if (same) B = A;
     else SG_TRY(gather_operand(xb, dtype, d, idb, mb, prec, metric, SIDE_B, cv, &B, st));
@@ -277,7 +293,8 @@ static size_t build_ws(uint64_t m, uint32_t d, sg_dtype dtype, const sg_build_pa
     size_t b = 1024;
     b += 2 * (m * p->L * 4 + 256);     // kNN ids + dists (when not caller-provided)
     b += 2 * (m * p->R * 4 + 256);     // pruned ids + dists
-    size_t knn = operand_bytes(prec, p->metric, d, m, SIDE_A | SIDE_B) + knn_core_workspace(p->L) + 1024;
+    size_t knn = 2 * (m * 4 + 256) + operand_bytes(prec, p->metric, d, m, SIDE_A | SIDE_B) + knn_core_workspace(p->L) +
+                 order_workspace(m, d, prec, p->metric) + 1024;
     size_t rev = reverse_ws(m, p->R);
     return b + (knn > rev ? knn : rev);
 }
@@ -333,10 +350,18 @@ sg_status scalegann_build_shard(const void* x, sg_dtype dtype, uint64_t n, uint3
     if (e != SG_OK) return e;
     SG_TRY(check_knn_shape(prec, p->metric, d, p->L));
     {
-        Carver kc = cv;   // the kNN scratch is reused by the reverse stage afterwards
+        // a4 gather in spatial order (order.cu) + a5 exact kNN; the scratch is reused by a6/a7
+        Carver kc = cv;
+        uint32_t* perm = kc.take<uint32_t>(m);
+        uint32_t* ids_perm = kc.take<uint32_t>(m);
+        if (!kc.ok()) { set_error("build: workspace too small"); return SG_ERR_WORKSPACE; }
+        const bool ordered = order_groups(m) >= 2;
+        if (ordered) SG_TRY(spatial_order(x, dtype, d, idmap, m, prec, p->metric, perm, ids_perm, kc, st));
         Operand A;
-        SG_TRY(gather_operand(x, dtype, d, idmap, m, prec, p->metric, SIDE_A | SIDE_B, kc, &A, st));
-        SG_TRY(knn_core(A, A, p->metric, true, p->L, kid, kd, nullptr, kc, st));
+        SG_TRY(gather_operand(x, dtype, d, ordered ? ids_perm : idmap, m, prec, p->metric, SIDE_A | SIDE_B, kc, &A,
+                              st));
+        SG_TRY(knn_core(A, A, p->metric, true, p->L, kid, kd, nullptr, kc, st, ordered ? perm : nullptr,
+                        ordered ? perm : nullptr, ordered));
     }
     SG_TRY(launch_prune(kid, kd, m, p->L, p->R, p->prune_rule, pr, prd, st));
     const uint32_t h = p->protected_edges ? p->protected_edges : p->R / 2;

@@ -27,6 +27,7 @@
 //   block the two halves of each row are merged and sorted by (dist, id).
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -40,6 +41,7 @@ constexpr uint32_t SLOT = ATOM;          // B ring slot
 constexpr uint32_t NEPI = 8;             // epilogue warps
 constexpr uint32_t NTHREADS = 64 + NEPI * 32;
 constexpr uint32_t MAX_STAGES = 16;
+constexpr uint32_t NBUF = 4;           // TMEM accumulator buffers (4 x 128 columns = all of TMEM)
 constexpr uint32_t KSTRIDE = 36;         // floats per staged row (16B aligned, conflict-free)
 constexpr uint32_t SCRATCH = 32 * KSTRIDE * 4;   // per epilogue warp: staged keys | hist | sort buffer
 
@@ -146,14 +148,26 @@ struct KnnParams {
     uint32_t* out_ids;     // ma x L
     float* out_d;          // ma x L
     float* probe;          // optional raw accumulator dump (ma x mb)
+    unsigned long long* prof;   // optional per-warp cycle counters (diagnostics)
+    const uint32_t* row_map;   // A row (operand order) -> output row (nullptr = identity)
+    const uint32_t* col_map;   // B row (operand order) -> reported id (nullptr = identity)
     uint32_t ma, mb, L, C, n_rb, n_ct, stages;
+    uint32_t t_back;           // with rotate: a row block starts t_back tiles before its diagonal
+    int rotate;                // column tiles visited from (rb - t_back) cyclically
     int self_exclude;
+    int noepi;                 // diagnostics: epilogue only drains TMEM (pipeline speed test)
 };
+
+__device__ __forceinline__ uint32_t tile_at(const KnnParams& p, uint32_t rb, uint32_t i) {
+    if (!p.rotate) return i;
+    const uint32_t back = p.t_back % p.n_ct;
+    return (rb + p.n_ct - back + i) % p.n_ct;
+}
 
 struct __align__(8) Bars {
     uint64_t full[MAX_STAGES], empty[MAX_STAGES];
     uint64_t a_full, a_empty;
-    uint64_t tm_full[2], tm_empty[2];
+    uint64_t tm_full[NBUF], tm_empty[NBUF];
     uint32_t tmem_base;
 };
 
@@ -170,7 +184,8 @@ __device__ __forceinline__ uint64_t ord2raw(uint64_t w) {
 }
 
 template <int EPL>
-__device__ uint32_t select_L(uint64_t* rb, uint32_t cnt, uint32_t L, uint32_t* hist, uint32_t lane) {
+__device__ uint32_t select_L(uint64_t* rb, uint32_t cnt, uint32_t L, uint32_t keep_max, uint32_t* hist,
+                         uint32_t lane, uint32_t* kept) {
     uint64_t e[EPL];
 #pragma unroll
     for (int i = 0; i < EPL; i++) {
@@ -210,7 +225,7 @@ __device__ uint32_t select_L(uint64_t* rb, uint32_t cnt, uint32_t L, uint32_t* h
         want -= before;
         pfx |= (uint64_t)dg << sh;
         __syncwarp();
-        if (bc == want) { cut = sh; break; }
+        if (L - want + bc <= keep_max) { cut = sh; *kept = L - want + bc; break; }
     }
     const uint64_t lim = pfx >> cut;
     uint32_t base = 0, mk = 0;
@@ -278,12 +293,13 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     uint8_t* scratch_all = (uint8_t*)(s_cnt + 2 * BM);     // NEPI x SCRATCH (16B aligned)
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    long long pw[6] = {0, 0, 0, 0, 0, 0};   // cycle counters (diagnostics)
 
     if (threadIdx.x == 0) {
         for (uint32_t s = 0; s < p.stages; s++) { mbar_init(&bars->full[s], 1); mbar_init(&bars->empty[s], 1); }
         mbar_init(&bars->a_full, 1);
         mbar_init(&bars->a_empty, 1);
-        for (int b = 0; b < 2; b++) { mbar_init(&bars->tm_full[b], 1); mbar_init(&bars->tm_empty[b], NEPI); }
+        for (uint32_t b = 0; b < NBUF; b++) { mbar_init(&bars->tm_full[b], 1); mbar_init(&bars->tm_empty[b], NEPI); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -297,7 +313,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&bars->tmem_base)),
-                     "r"(256u));
+                     "r"(NBUF * BN));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
@@ -314,10 +330,13 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 mbar_expect_tx(&bars->a_full, NKA * ATOM + (MINI ? MINIB : 0u));
                 for (int ka = 0; ka < NKA; ka++) tma_load_2d(&tmA, &bars->a_full, sA + ka * ATOM, ka * ATOM_K, rb * BM);
                 if (MINI) tma_load_2d(&tmAm, &bars->a_full, sAm, NKA * ATOM_K, rb * BM);
-                for (uint32_t t = 0; t < p.n_ct; t++) {
+                for (uint32_t ti = 0; ti < p.n_ct; ti++) {
+                    const uint32_t t = tile_at(p, rb, ti);
 #pragma unroll
                     for (uint32_t ka = 0; ka < NSLOT; ka++) {
+                        const long long w0 = clock64();
                         mbar_wait(&bars->empty[stage], sph ^ 1);
+                        pw[0] += clock64() - w0;
                         if (ka < NKA) {
                             mbar_expect_tx(&bars->full[stage], ATOM);
                             tma_load_2d(&tmB, &bars->full[stage], sB + stage * SLOT, ka * ATOM_K, t * BN);
@@ -339,14 +358,18 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             for (uint32_t rb = blockIdx.x; rb < p.n_rb; rb += gridDim.x, it++) {
                 mbar_wait(&bars->a_full, it & 1);
                 tc_fence_after();
-                for (uint32_t t = 0; t < p.n_ct; t++, git++) {
-                    const uint32_t buf = git & 1;
-                    mbar_wait(&bars->tm_empty[buf], ((git >> 1) & 1) ^ 1);
+                for (uint32_t ti = 0; ti < p.n_ct; ti++, git++) {
+                    const uint32_t buf = git % NBUF;
+                    const long long w0 = clock64();
+                    mbar_wait(&bars->tm_empty[buf], ((git / NBUF) & 1) ^ 1);
+                    pw[0] += clock64() - w0;
                     tc_fence_after();
                     const uint32_t dcol = tmem + buf * BN;
 #pragma unroll
                     for (uint32_t ka = 0; ka < NSLOT; ka++) {
+                        const long long w1 = clock64();
                         mbar_wait(&bars->full[stage], sph);
+                        pw[1] += clock64() - w1;
                         tc_fence_after();
                         if (ka < NKA) {
 #pragma unroll
@@ -366,6 +389,10 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         }
     } else {
         // ===================== epilogue: fused selection =====================
+        // warp e: TMEM lane quadrant q (rows q*32..q*32+31), column half h of every tile.
+        // The two warps of a quadrant share one candidate buffer per row (slots from a
+        // shared-memory count) and meet at a named barrier at every tile boundary, where rows
+        // whose buffer might overflow are compacted (split between the two warps).
         const uint32_t e = warp - 2, q = warp & 3, h = e >> 2;
         const uint32_t r = q * 32 + lane;                    // row within the block
         uint8_t* scratch = scratch_all + e * SCRATCH;
@@ -373,22 +400,24 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         uint32_t* hist = (uint32_t*)scratch;                 // 256 (aliases skeys)
         uint64_t* sortbuf = (uint64_t*)scratch;              // 512 (aliases skeys)
         const uint32_t C = p.C;
-        uint64_t* half_base = p.cand + ((uint64_t)blockIdx.x * 2 + h) * BM * C;
-        uint64_t* myrow = half_base + (uint64_t)r * C;
-        uint64_t* warprows = half_base + (uint64_t)q * 32 * C;
+        const uint32_t keep_max = p.L + (C - 128 - p.L) / 4;   // approximate in-loop compaction target
+        uint64_t* cta_base = p.cand + (uint64_t)blockIdx.x * BM * C;
+        uint64_t* myrow = cta_base + (uint64_t)r * C;
+        uint64_t* quadrows = cta_base + (uint64_t)q * 32 * C;
         const float INF = __int_as_float(0x7f800000);
         const uint32_t tl = tmem + ((q * 32) << 16) + h * 64;
         uint32_t git = 0;
         for (uint32_t rb = blockIdx.x; rb < p.n_rb; rb += gridDim.x) {
             const uint32_t row = rb * BM + r;
             const bool valid = row < p.ma;
-            float thr = valid ? INF : -INF;
-            uint32_t cnt = 0;
-            s_thr[h * BM + r] = thr;
-            named_bar_sync(1 + q, 64);
-            for (uint32_t t = 0; t < p.n_ct; t++, git++) {
-                const uint32_t buf = git & 1;
-                mbar_wait(&bars->tm_full[buf], (git >> 1) & 1);
+            if (h == 0) { s_thr[r] = valid ? INF : -INF; s_cnt[r] = 0; }
+            for (uint32_t ti = 0; ti < p.n_ct; ti++, git++) {
+                const uint32_t t = tile_at(p, rb, ti);
+                const uint32_t buf = git % NBUF;
+                long long c0 = clock64();
+                mbar_wait(&bars->tm_full[buf], (git / NBUF) & 1);
+                long long c1 = clock64();
+                pw[0] += c1 - c0;
                 tc_fence_after();
                 const uint32_t tb = tl + buf * BN;
                 uint32_t v[2][32];
@@ -399,6 +428,10 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->tm_empty[buf]);   // accumulator now in registers
                 const uint32_t colh = t * BN + h * 64;
+                if (p.noepi) {
+                    if (v[0][lane] == 0x7fc00001u) p.out_ids[0] = v[1][lane];   // keep the loads live
+                    continue;
+                }
                 if (p.probe) {
                     if (valid)
                         for (int ch = 0; ch < 2; ch++)
@@ -407,86 +440,107 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                                     p.probe[(uint64_t)row * p.mb + colh + ch * 32 + j] = __uint_as_float(v[ch][j]);
                     continue;
                 }
-                // make room: rows whose buffer cannot take another 64 candidates are compacted
-                uint32_t need = __ballot_sync(0xffffffffu, cnt > C - 64);
-                while (need) {
-                    const int o = __ffs(need) - 1;
-                    need &= need - 1;
-                    const uint32_t c_o = __shfl_sync(0xffffffffu, cnt, o);
-                    const uint32_t kth = select_L<EPL>(warprows + (uint64_t)o * C, c_o, p.L, hist, lane);
-                    if (lane == (uint32_t)o) {
-                        cnt = p.L;
-                        thr = ord2f(kth);
-                        s_thr[h * BM + r] = thr;
+                named_bar_sync(1 + q, 64);               // both halves finished the previous tile
+                c0 = clock64();
+                pw[1] += c0 - c1;
+                // rows whose buffer cannot take this tile's <= 128 candidates are compacted
+                uint32_t need = __ballot_sync(0xffffffffu, s_cnt[r] > C - 128);
+                if (need) {
+                    uint32_t mine = need & (h ? 0xAAAAAAAAu : 0x55555555u);
+                    while (mine) {
+                        const int o = __ffs(mine) - 1;
+                        mine &= mine - 1;
+                        uint32_t kept;
+                        const uint32_t kth = select_L<EPL>(quadrows + (uint64_t)o * C, s_cnt[q * 32 + o], p.L, keep_max,
+                                                           hist, lane, &kept);
+                        if (lane == 0) { s_cnt[q * 32 + o] = kept; s_thr[q * 32 + o] = ord2f(kth); }
                     }
+                    __syncwarp();
+                    named_bar_sync(1 + q, 64);
                 }
-                const float te = fminf(thr, next_up(s_thr[(h ^ 1) * BM + r]));
-                // pass masks: bit j = sign(key_j - te)  (key < te; NaN / equal -> 0), two
-                // subtractions per FADD2, one funnel shift per element
+                c1 = clock64();
+                pw[2] += c1 - c0;   // compaction
+                // inclusive test: the row's columns reach the buffer out of id order (two halves,
+                // rotated sweep), so ties are resolved by the exact selection at the end
+                const float te = next_up(s_thr[r]);
+                // pass masks: bit j = sign(key_j - te) (key < te; NaN / equal -> 0)
                 uint32_t mk[2];
 #pragma unroll
                 for (int ch = 0; ch < 2; ch++) {
-                    uint32_t m = 0;
+                    uint32_t mq[4] = {0, 0, 0, 0};
 #pragma unroll
-                    for (int j = 31; j >= 1; j -= 2) {
-                        uint32_t lo, hi;
-                        sub2(v[ch][j - 1], v[ch][j], te, lo, hi);
-                        m = __funnelshift_l(hi, m, 1);
-                        m = __funnelshift_l(lo, m, 1);
+                    for (int s = 7; s >= 1; s -= 2) {
+#pragma unroll
+                        for (int g = 0; g < 4; g++) {
+                            const int j = g * 8 + s;
+                            uint32_t lo, hi;
+                            sub2(v[ch][j - 1], v[ch][j], te, lo, hi);
+                            mq[g] = __funnelshift_l(hi, mq[g], 1);
+                            mq[g] = __funnelshift_l(lo, mq[g], 1);
+                        }
                     }
-                    mk[ch] = m;
+                    mk[ch] = mq[0] | (mq[1] << 8) | (mq[2] << 16) | (mq[3] << 24);
                 }
                 if (p.self_exclude && t == rb && (q >> 1) == h) mk[q & 1] &= ~(1u << lane);   // self column
+                c0 = clock64();
+                pw[3] += c0 - c1;   // masks
                 if (__any_sync(0xffffffffu, (mk[0] | mk[1]) != 0)) {
+                    const uint32_t np = __popc(mk[0]) + __popc(mk[1]);
+                    uint32_t slot = np ? atomicAdd(&s_cnt[r], np) : 0;
 #pragma unroll
                     for (int ch = 0; ch < 2; ch++) {
                         uint32_t m = mk[ch];
                         if (!__any_sync(0xffffffffu, m != 0)) continue;
-                        float4* mine = (float4*)(skeys + lane * KSTRIDE);
+                        float4* st4 = (float4*)(skeys + lane * KSTRIDE);
 #pragma unroll
                         for (int j4 = 0; j4 < 8; j4++)
-                            mine[j4] = make_float4(__uint_as_float(v[ch][4 * j4]), __uint_as_float(v[ch][4 * j4 + 1]),
-                                                   __uint_as_float(v[ch][4 * j4 + 2]),
-                                                   __uint_as_float(v[ch][4 * j4 + 3]));
+                            st4[j4] = make_float4(__uint_as_float(v[ch][4 * j4]), __uint_as_float(v[ch][4 * j4 + 1]),
+                                                  __uint_as_float(v[ch][4 * j4 + 2]),
+                                                  __uint_as_float(v[ch][4 * j4 + 3]));
                         __syncwarp();
                         const uint32_t cb = colh + ch * 32;
                         while (m) {
                             const uint32_t c = 31 - __clz(m);
                             m ^= 1u << c;
                             const uint32_t kb = __float_as_uint(skeys[lane * KSTRIDE + c]);
-                            myrow[cnt++] = ((uint64_t)kb << 32) | (cb + c);
+                            const uint32_t id = p.col_map ? __ldg(p.col_map + cb + c) : cb + c;
+                            myrow[slot++] = ((uint64_t)kb << 32) | id;
                         }
                         __syncwarp();
                     }
                 }
+                pw[4] += clock64() - c0;   // insertions
             }
-            if (p.probe) continue;
-            // ---- final: each half keeps its exact top-L, then the two halves of a row are merged
-            __syncwarp();
-            for (uint32_t o = 0; o < 32; o++) {
-                uint32_t c_o = __shfl_sync(0xffffffffu, cnt, o);
-                if (c_o > p.L) { select_L<EPL>(warprows + (uint64_t)o * C, c_o, p.L, hist, lane); c_o = p.L; }
-                if (lane == 0) s_cnt[h * BM + q * 32 + o] = c_o;
-            }
-            __syncwarp();
+            if (p.probe || p.noepi) continue;
+            const long long f0 = clock64();
+            // ---- final: exact top-L of each row sorted by (dist, id); rows split between the halves
             named_bar_sync(1 + q, 64);
             for (uint32_t i = 0; i < 16; i++) {
                 const uint32_t rr = q * 32 + h * 16 + i;
                 const uint32_t row_o = rb * BM + rr;
                 if (row_o >= p.ma) continue;
-                const uint64_t* b0 = p.cand + ((uint64_t)blockIdx.x * 2 + 0) * BM * C + (uint64_t)rr * C;
-                const uint64_t* b1 = p.cand + ((uint64_t)blockIdx.x * 2 + 1) * BM * C + (uint64_t)rr * C;
-                finish_row(b0, s_cnt[rr], b1, s_cnt[BM + rr], p.L, sortbuf, p.norm_a[row_o],
-                           p.out_ids + (uint64_t)row_o * p.L, p.out_d + (uint64_t)row_o * p.L, lane);
+                uint64_t* b0 = cta_base + (uint64_t)rr * C;
+                uint32_t c_o = s_cnt[rr];
+                if (c_o > p.L) {
+                    uint32_t kept;
+                    select_L<EPL>(b0, c_o, p.L, p.L, hist, lane, &kept);
+                    c_o = p.L;
+                }
+                const uint64_t orow = p.row_map ? p.row_map[row_o] : row_o;
+                finish_row(b0, c_o, b0, 0, p.L, sortbuf, p.norm_a[row_o], p.out_ids + orow * p.L,
+                           p.out_d + orow * p.L, lane);
             }
             named_bar_sync(1 + q, 64);
+            pw[5] += clock64() - f0;   // final phase
         }
     }
+    if (p.prof && lane == 0)
+        for (int i = 0; i < 6; i++) atomicAdd(p.prof + warp * 8 + i, (unsigned long long)pw[i]);
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256u));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(NBUF * BN));
     }
 }
 
@@ -520,7 +574,7 @@ sg_status make_map(CUtensorMap* m, const void* base, uint64_t rows, uint32_t kdi
 }
 
 uint32_t cand_cap(uint32_t L) {
-    uint32_t c = 128;
+    uint32_t c = 256;   // > 128 + L: room for one tile of candidates above the kept set
     while (c < 4 * L && c < 1024) c <<= 1;
     return c;
 }
@@ -566,12 +620,16 @@ sg_status launch_mini(int nka, int mini, const CUtensorMap* maps, KnnParams& p, 
 
 }  // namespace
 
+unsigned long long* g_knn_prof = nullptr;
+void set_knn_profile(unsigned long long* buf) { g_knn_prof = buf; }
+
 size_t knn_core_workspace(uint32_t L) {
     return (size_t)num_sms() * 2 * BM * cand_cap(L) * sizeof(uint64_t) + 4096;
 }
 
 sg_status knn_core(const Operand& A, const Operand& B, int /*metric*/, bool self_exclude, uint32_t L, uint32_t* ids,
-                   float* dists, float* probe, Carver& cv, cudaStream_t st) {
+                   float* dists, float* probe, Carver& cv, cudaStream_t st, const uint32_t* row_map,
+                   const uint32_t* col_map, bool rotate) {
     if (A.kdim != B.kdim || A.esize != B.esize || A.nfull != B.nfull || A.mini != B.mini) {
         set_error("kNN: operand layout mismatch");
         return SG_ERR_INVALID_ARG;
@@ -584,12 +642,24 @@ sg_status knn_core(const Operand& A, const Operand& B, int /*metric*/, bool self
     p.out_ids = ids;
     p.out_d = dists;
     p.probe = probe;
+    p.prof = g_knn_prof;
     p.ma = (uint32_t)A.rows;
     p.mb = (uint32_t)B.rows;
     p.L = L;
     p.n_rb = (uint32_t)(A.rows_pad / BM);
     p.n_ct = (uint32_t)(B.rows_pad / BN);
     p.self_exclude = self_exclude ? 1 : 0;
+    p.row_map = row_map;
+    p.col_map = col_map;
+    p.rotate = rotate ? 1 : 0;
+    {
+        static int tb = -1;
+        if (tb < 0) { const char* e = getenv("SG_TBACK"); tb = e ? atoi(e) : 4; }
+        p.t_back = (uint32_t)tb;
+        static int ne = -1;
+        if (ne < 0) { const char* e = getenv("SG_KNN_NOEPI"); ne = e ? atoi(e) : 0; }
+        p.noepi = ne;
+    }
     CUtensorMap maps[4];
     SG_TRY(make_map(&maps[0], A.a, A.rows_pad, A.kdim, A.esize, 128));
     SG_TRY(make_map(&maps[1], B.b, B.rows_pad, B.kdim, B.esize, 128));
@@ -603,11 +673,11 @@ sg_status knn_core(const Operand& A, const Operand& B, int /*metric*/, bool self
     const int epl = (int)(p.C / 32);
     const int nka = (int)A.nfull, mini = (int)A.mini;
     if (A.esize == 4) {
-        if (epl <= 4) return launch_mini<1, 4>(nka, mini, maps, p, st);
+        if (epl <= 8) return launch_mini<1, 8>(nka, mini, maps, p, st);
         if (epl <= 16) return launch_mini<1, 16>(nka, mini, maps, p, st);
         return launch_mini<1, 32>(nka, mini, maps, p, st);
     }
-    if (epl <= 4) return launch_mini<0, 4>(nka, mini, maps, p, st);
+    if (epl <= 8) return launch_mini<0, 8>(nka, mini, maps, p, st);
     if (epl <= 16) return launch_mini<0, 16>(nka, mini, maps, p, st);
     return launch_mini<0, 32>(nka, mini, maps, p, st);
 }

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--kind", default="sift")
     ap.add_argument("--precision", type=int, default=0)
+    ap.add_argument("--prof", action="store_true")
     a = ap.parse_args()
     api.load()
     x = (datagen.sift_like(a.m, a.d, device="cuda") if a.kind == "sift"
@@ -38,6 +39,17 @@ def main():
         api.scalegann_knn(x, a.L, precision=a.precision, ws=ws)
     torch.cuda.synchronize()
     ms, nl, _ = api.scalegann_stats_read(reset=True)
+    if a.prof:
+        cnt = torch.zeros(80, dtype=torch.int64, device="cuda")
+        api.scalegann_knn_profile(cnt)
+        api.scalegann_knn(x, a.L, precision=a.precision, ws=ws)
+        torch.cuda.synchronize()
+        api.scalegann_knn_profile(None)
+        c = cnt.view(10, 8)[:, :6].double().cpu()
+        names = ["wait", "tmem/full", "compact", "mask", "insert", "final"]
+        tot = c.sum(1, keepdim=True)
+        for w in range(10):
+            print(f"warp {w}: " + " ".join(f"{n}={v / 1e9:.2f}G" for n, v in zip(names, c[w].tolist())))
     per = ms / max(nl, 1)
     fl = 2.0 * a.m * a.m * a.d
     print(json.dumps({"m": a.m, "d": a.d, "L": a.L, "ms_per_launch": per, "tflops": fl / (per / 1e3) / 1e12}))
