@@ -146,7 +146,7 @@ void operand_layout(int prec, int metric, uint32_t d, uint32_t* kdim, uint32_t* 
 size_t operand_bytes(int prec, int metric, uint32_t d, uint64_t rows, int sides) {
     uint32_t kdim, nf, mi;
     operand_layout(prec, metric, d, &kdim, &nf, &mi);
-    const uint64_t rp = (rows + 127) / 128 * 128;
+    const uint64_t rp = (rows + 255) / 256 * 256;   // multiple of the distance kernel row block
     const size_t e = prec == SG_PREC_F16_EXACT ? 2 : 4;
     const int ns = ((sides & SIDE_A) ? 1 : 0) + ((sides & SIDE_B) ? 1 : 0);
     return ns * (rp * kdim * e + 256) + rp * sizeof(float) + 1024;
@@ -176,7 +176,7 @@ sg_status gather_operand(const void* x, sg_dtype dtype, uint32_t d, const uint32
     operand_layout(prec, metric, d, &op->kdim, &op->nfull, &op->mini);
     op->esize = prec == SG_PREC_F16_EXACT ? 2 : 4;
     op->rows = m;
-    op->rows_pad = (m + 127) / 128 * 128;
+    op->rows_pad = (m + 255) / 256 * 256;   // multiple of the distance kernel row block (256)
     const size_t elems = op->rows_pad * op->kdim;
     op->a = (sides & SIDE_A) ? cv.take<uint8_t>(elems * op->esize) : nullptr;
     op->b = (sides & SIDE_B) ? cv.take<uint8_t>(elems * op->esize) : nullptr;

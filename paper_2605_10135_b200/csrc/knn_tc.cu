@@ -7,24 +7,22 @@
 // the tensor-core accumulator IS the key (exact in fp32 for integer data: every partial sum is
 // an integer below 2^24).  dist = |a_i|^2 + key is formed once per output.
 //
-// Pipeline (persistent, one CTA per SM, 10 warps):
-//   warp 0: TMA producer — A row block (128 rows x K, resident in smem: NKA 128B-swizzle atoms
-//           + an optional 32B-swizzle "mini" atom holding the K tail) and the B column tiles
-//           through a ring of 16 KB slots; every CTA walks the columns in the same order so
-//           the B stream is served from L2.
-//   warp 1: TMEM allocator + single-thread tcgen05.mma issuer (kind::f16 / kind::tf32,
-//           M=128, N=128, fp32 accumulate) into a double-buffered TMEM accumulator.
-//   warps 2..9: epilogue; warp e reads TMEM lane quadrant q = warp%4 (32 rows) and column
-//           half h = e/4 (64 of the 128 columns) of every tile.  Per 32-column chunk a thread
-//           (= one row) builds a pass mask with FADD + funnel shift (sign of key - thr, 2
-//           instructions per element); only set bits are appended, as (ord(key) << 32 | col),
-//           to the row's candidate buffer (global memory, L2 resident), reading the keys back
-//           from a shared-memory stage.  Columns of a half arrive in increasing id, so the
-//           strict test realises the (dist, id) order; each half also filters with the other
-//           half's threshold (inclusive, nextup) which keeps exactness.
-//   When a buffer nears full its warp radix-selects the exact L smallest (8-bit digits,
-//   shared-memory histogram) and lowers the threshold to the L-th key.  At the end of a row
-//   block the two halves of each row are merged and sorted by (dist, id).
+// Pipeline (persistent, one CTA per SM, 10 warps).  A CTA owns a 256-row block held resident
+// in shared memory as two 128-row halves (NKA 128B-swizzle atoms + an optional 32B-swizzle
+// "mini" atom for the K tail each); every 64-column B tile streamed in is used by BOTH halves
+// (two M=128, N=64 MMAs), which halves the operand bytes per flop that L2 must deliver.
+//   warp 0: TMA producer (A block, then the B tiles through a ring of 8 KB slots; the column
+//           sweep of a row block starts t_back tiles before its diagonal when the shard is in
+//           spatial order, so the row's neighbourhood is seen first).
+//   warp 1: TMEM allocator + single-thread tcgen05.mma issuer, accumulators
+//           [half a][buffer b] = 64 TMEM columns each, 2 x 4 buffers = all 512 columns.
+//   warps 2..9: epilogue; warp (q, a) owns rows a*128 + q*32 + lane (TMEM lane quadrant q of
+//           accumulator a).  Per tile a thread (= one row) builds a 64-bit pass mask with FADD2
+//           + funnel shifts (sign of key - threshold, 1.5 instructions per element) and appends
+//           only set bits, as (key bits << 32 | id), to its row's candidate buffer (global, L2
+//           resident).  When a buffer nears full, the warp radix-selects (8-bit digits, smem
+//           histogram) a small superset of the L best and lowers the threshold; at the end of a
+//           row block the exact top-L is selected and sorted by (dist, id).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <stdlib.h>
@@ -34,16 +32,21 @@
 namespace sg {
 namespace {
 
-constexpr uint32_t BM = 128, BN = 128;
-constexpr uint32_t ATOM = 128 * 128;     // 128 rows x 128 B (128B swizzle)
-constexpr uint32_t MINIB = 128 * 32;     // 128 rows x 32 B (32B swizzle)
-constexpr uint32_t SLOT = ATOM;          // B ring slot
+constexpr uint32_t MSUB = 128;           // rows per accumulator (MMA M)
+constexpr uint32_t NACC = 2;             // accumulators (row halves) per CTA
+constexpr uint32_t BM = MSUB * NACC;     // rows per CTA row block
+constexpr uint32_t BN = 64;              // columns per tile (MMA N)
+constexpr uint32_t ATOM = 128 * 128;     // A atom: 128 rows x 128 B (128B swizzle)
+constexpr uint32_t MINIB = 128 * 32;     // A mini atom: 128 rows x 32 B (32B swizzle)
+constexpr uint32_t BATOM = BN * 128;     // B atom: 64 rows x 128 B
+constexpr uint32_t BMINI = BN * 32;      // B mini atom: 64 rows x 32 B
+constexpr uint32_t SLOT = BATOM;         // B ring slot
 constexpr uint32_t NEPI = 8;             // epilogue warps
 constexpr uint32_t NTHREADS = 64 + NEPI * 32;
-constexpr uint32_t MAX_STAGES = 16;
-constexpr uint32_t NBUF = 4;           // TMEM accumulator buffers (4 x 128 columns = all of TMEM)
+constexpr uint32_t MAX_STAGES = 32;
+constexpr uint32_t NBUF = 4;             // TMEM buffers per accumulator (2 x 4 x 64 = 512 columns)
 constexpr uint32_t KSTRIDE = 36;         // floats per staged row (16B aligned, conflict-free)
-constexpr uint32_t SCRATCH = 32 * KSTRIDE * 4;   // per epilogue warp: staged keys | hist | sort buffer
+constexpr uint32_t SCRATCH = 32 * KSTRIDE * 4 + 64 * 4;   // per warp: staged keys | hist | sort buffer, + tile ids
 
 // ----------------------------------------------------------------- PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -121,10 +124,10 @@ __device__ __forceinline__ uint64_t desc_sw32(uint32_t saddr) {
     return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)(256u >> 4) << 32) | (1ull << 46) | (6ull << 61);
 }
 
-// Instruction descriptor: D fp32, A/B f16 (KIND 0) or tf32 (KIND 1), both K-major, M=128, N=128.
+// Instruction descriptor: D fp32, A/B f16 (KIND 0) or tf32 (KIND 1), both K-major, M=128, N=BN.
 template <int KIND>
 __host__ __device__ constexpr uint32_t instr_desc() {
-    return (1u << 4) | ((KIND ? 2u : 0u) << 7) | ((KIND ? 2u : 0u) << 10) | ((BN >> 3) << 17) | ((BM >> 4) << 24);
+    return (1u << 4) | ((KIND ? 2u : 0u) << 7) | ((KIND ? 2u : 0u) << 10) | ((BN >> 3) << 17) | ((MSUB >> 4) << 24);
 }
 
 // (a - t, b - t) with one packed FADD2 (sm_100); results as raw bits
@@ -143,25 +146,26 @@ __device__ __forceinline__ float next_up(float x) {   // smallest float > x (x <
 }
 
 struct KnnParams {
-    const float* norm_a;   // |a_i|^2 (0 for IP) for the final distance
-    uint64_t* cand;        // gridDim.x * 2 halves * 128 rows * C candidate words
-    uint32_t* out_ids;     // ma x L
-    float* out_d;          // ma x L
-    float* probe;          // optional raw accumulator dump (ma x mb)
-    unsigned long long* prof;   // optional per-warp cycle counters (diagnostics)
+    const float* norm_a;       // |a_i|^2 (0 for IP) for the final distance, operand row order
+    uint64_t* cand;            // gridDim.x * BM rows * C candidate words
+    uint32_t* out_ids;         // ma x L
+    float* out_d;              // ma x L
+    float* probe;              // optional raw accumulator dump (ma x mb)
+    unsigned long long* prof;  // optional per-warp cycle counters (diagnostics)
     const uint32_t* row_map;   // A row (operand order) -> output row (nullptr = identity)
     const uint32_t* col_map;   // B row (operand order) -> reported id (nullptr = identity)
     uint32_t ma, mb, L, C, n_rb, n_ct, stages;
     uint32_t t_back;           // with rotate: a row block starts t_back tiles before its diagonal
-    int rotate;                // column tiles visited from (rb - t_back) cyclically
+    int rotate;                // column tiles visited from the diagonal - t_back cyclically
     int self_exclude;
     int noepi;                 // diagnostics: epilogue only drains TMEM (pipeline speed test)
 };
 
 __device__ __forceinline__ uint32_t tile_at(const KnnParams& p, uint32_t rb, uint32_t i) {
     if (!p.rotate) return i;
+    const uint32_t diag = rb * (BM / BN) % p.n_ct;
     const uint32_t back = p.t_back % p.n_ct;
-    return (rb + p.n_ct - back + i) % p.n_ct;
+    return (diag + p.n_ct - back + i) % p.n_ct;
 }
 
 struct __align__(8) Bars {
@@ -171,9 +175,6 @@ struct __align__(8) Bars {
     uint32_t tmem_base;
 };
 
-// ----------------------------------------------------------------- top-L selection
-// Warp-cooperative: keep exactly the L smallest of rb[0..cnt) (in place at rb[0..L)) and
-// return the L-th key (ordered u32).  All 32 lanes call with the same arguments.
 // Candidate words are stored raw as (float bits << 32 | col); selection works on the ordered
 // form (ord(key) << 32 | col) whose unsigned order is the (key, col) order.
 __device__ __forceinline__ uint64_t raw2ord(uint64_t w) {
@@ -282,18 +283,15 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     constexpr uint32_t EL = KIND ? 4 : 2;                  // bytes per element
     constexpr uint32_t ATOM_K = 128 / EL;                  // elements per 128B atom
     constexpr uint32_t NSLOT = NKA + MINI;                 // ring slots per column tile
-    constexpr uint32_t A_BYTES = NKA * ATOM + (MINI ? 1024u * ((MINIB + 1023) / 1024) : 0u);
+    constexpr uint32_t AHALF = NKA * ATOM + (MINI ? MINIB : 0u);   // bytes of one 128-row half
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint8_t* sA = smem;
-    uint8_t* sAm = smem + NKA * ATOM;
-    uint8_t* sB = smem + A_BYTES;
+    uint8_t* sA = smem;                                    // [NACC][NKA atoms + mini]
+    uint8_t* sB = smem + NACC * AHALF;
     Bars* bars = (Bars*)(sB + p.stages * SLOT);
-    float* s_thr = (float*)(((uintptr_t)(bars + 1) + 127) & ~(uintptr_t)127);   // 2 halves x 128 rows
-    uint32_t* s_cnt = (uint32_t*)(s_thr + 2 * BM);         // 2 halves x 128 rows
-    uint8_t* scratch_all = (uint8_t*)(s_cnt + 2 * BM);     // NEPI x SCRATCH (16B aligned)
+    uint8_t* scratch_all = (uint8_t*)(((uintptr_t)(bars + 1) + 127) & ~(uintptr_t)127);   // NEPI x SCRATCH
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    long long pw[6] = {0, 0, 0, 0, 0, 0};   // cycle counters (diagnostics)
+    long long pw[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // cycle counters + event counts (diagnostics)
 
     if (threadIdx.x == 0) {
         for (uint32_t s = 0; s < p.stages; s++) { mbar_init(&bars->full[s], 1); mbar_init(&bars->empty[s], 1); }
@@ -313,7 +311,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&bars->tmem_base)),
-                     "r"(NBUF * BN));
+                     "r"(512u));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
@@ -327,25 +325,29 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             uint32_t stage = 0, sph = 0, it = 0;
             for (uint32_t rb = blockIdx.x; rb < p.n_rb; rb += gridDim.x, it++) {
                 if (it > 0) mbar_wait(&bars->a_empty, (it - 1) & 1);
-                mbar_expect_tx(&bars->a_full, NKA * ATOM + (MINI ? MINIB : 0u));
-                for (int ka = 0; ka < NKA; ka++) tma_load_2d(&tmA, &bars->a_full, sA + ka * ATOM, ka * ATOM_K, rb * BM);
-                if (MINI) tma_load_2d(&tmAm, &bars->a_full, sAm, NKA * ATOM_K, rb * BM);
+                mbar_expect_tx(&bars->a_full, NACC * AHALF);
+                for (uint32_t a = 0; a < NACC; a++) {
+                    uint8_t* base = sA + a * AHALF;
+                    for (int ka = 0; ka < NKA; ka++)
+                        tma_load_2d(&tmA, &bars->a_full, base + ka * ATOM, ka * ATOM_K, rb * BM + a * MSUB);
+                    if (MINI) tma_load_2d(&tmAm, &bars->a_full, base + NKA * ATOM, NKA * ATOM_K, rb * BM + a * MSUB);
+                }
                 for (uint32_t ti = 0; ti < p.n_ct; ti++) {
                     const uint32_t t = tile_at(p, rb, ti);
+                    long long w0 = clock64();
 #pragma unroll
                     for (uint32_t ka = 0; ka < NSLOT; ka++) {
-                        const long long w0 = clock64();
                         mbar_wait(&bars->empty[stage], sph ^ 1);
-                        pw[0] += clock64() - w0;
                         if (ka < NKA) {
-                            mbar_expect_tx(&bars->full[stage], ATOM);
+                            mbar_expect_tx(&bars->full[stage], BATOM);
                             tma_load_2d(&tmB, &bars->full[stage], sB + stage * SLOT, ka * ATOM_K, t * BN);
                         } else {
-                            mbar_expect_tx(&bars->full[stage], MINIB);
+                            mbar_expect_tx(&bars->full[stage], BMINI);
                             tma_load_2d(&tmBm, &bars->full[stage], sB + stage * SLOT, NKA * ATOM_K, t * BN);
                         }
                         if (++stage == p.stages) { stage = 0; sph ^= 1; }
                     }
+                    pw[0] += clock64() - w0;
                 }
             }
         }
@@ -353,7 +355,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         // ===================== MMA issuer =====================
         if (lane == 0) {
             constexpr uint32_t idesc = instr_desc<KIND>();
-            const uint32_t a_base = smem_u32(sA), am_base = smem_u32(sAm), b_base = smem_u32(sB);
+            const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
             uint32_t stage = 0, sph = 0, it = 0, git = 0;
             for (uint32_t rb = blockIdx.x; rb < p.n_rb; rb += gridDim.x, it++) {
                 mbar_wait(&bars->a_full, it & 1);
@@ -364,20 +366,25 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     mbar_wait(&bars->tm_empty[buf], ((git / NBUF) & 1) ^ 1);
                     pw[0] += clock64() - w0;
                     tc_fence_after();
-                    const uint32_t dcol = tmem + buf * BN;
 #pragma unroll
                     for (uint32_t ka = 0; ka < NSLOT; ka++) {
                         const long long w1 = clock64();
                         mbar_wait(&bars->full[stage], sph);
                         pw[1] += clock64() - w1;
                         tc_fence_after();
-                        if (ka < NKA) {
+                        const uint32_t bslot = b_base + stage * SLOT;
 #pragma unroll
-                            for (uint32_t kk = 0; kk < 4; kk++)
-                                tc_mma<KIND>(dcol, desc_sw128(a_base + ka * ATOM + kk * 32),
-                                             desc_sw128(b_base + stage * SLOT + kk * 32), idesc, (ka | kk) != 0);
-                        } else {
-                            tc_mma<KIND>(dcol, desc_sw32(am_base), desc_sw32(b_base + stage * SLOT), idesc, NKA != 0);
+                        for (uint32_t a = 0; a < NACC; a++) {
+                            const uint32_t dcol = tmem + (a * NBUF + buf) * BN;
+                            const uint32_t abase = a_base + a * AHALF;
+                            if (ka < NKA) {
+#pragma unroll
+                                for (uint32_t kk = 0; kk < 4; kk++)
+                                    tc_mma<KIND>(dcol, desc_sw128(abase + ka * ATOM + kk * 32), desc_sw128(bslot + kk * 32),
+                                                 idesc, (ka | kk) != 0);
+                            } else {
+                                tc_mma<KIND>(dcol, desc_sw32(abase + NKA * ATOM), desc_sw32(bslot), idesc, NKA != 0);
+                            }
                         }
                         tc_commit(&bars->empty[stage]);
                         if (++stage == p.stages) { stage = 0; sph ^= 1; }
@@ -389,28 +396,25 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         }
     } else {
         // ===================== epilogue: fused selection =====================
-        // warp e: TMEM lane quadrant q (rows q*32..q*32+31), column half h of every tile.
-        // The two warps of a quadrant share one candidate buffer per row (slots from a
-        // shared-memory count) and meet at a named barrier at every tile boundary, where rows
-        // whose buffer might overflow are compacted (split between the two warps).
-        const uint32_t e = warp - 2, q = warp & 3, h = e >> 2;
-        const uint32_t r = q * 32 + lane;                    // row within the block
+        const uint32_t e = warp - 2, q = warp & 3, a = e >> 2;
+        const uint32_t r = a * MSUB + q * 32 + lane;         // row within the block
         uint8_t* scratch = scratch_all + e * SCRATCH;
         float* skeys = (float*)scratch;                      // [32][KSTRIDE] staged keys
         uint32_t* hist = (uint32_t*)scratch;                 // 256 (aliases skeys)
         uint64_t* sortbuf = (uint64_t*)scratch;              // 512 (aliases skeys)
+        uint32_t* sids = (uint32_t*)(scratch + 32 * KSTRIDE * 4);   // 64 reported ids of the tile
         const uint32_t C = p.C;
-        const uint32_t keep_max = p.L + (C - 128 - p.L) / 4;   // approximate in-loop compaction target
-        uint64_t* cta_base = p.cand + (uint64_t)blockIdx.x * BM * C;
-        uint64_t* myrow = cta_base + (uint64_t)r * C;
-        uint64_t* quadrows = cta_base + (uint64_t)q * 32 * C;
+        const uint32_t keep_max = p.L + (C - BN - p.L) / 4;  // approximate in-loop compaction target
+        uint64_t* myrow = p.cand + ((uint64_t)blockIdx.x * BM + r) * C;
+        uint64_t* warprows = p.cand + ((uint64_t)blockIdx.x * BM + a * MSUB + q * 32) * C;
         const float INF = __int_as_float(0x7f800000);
-        const uint32_t tl = tmem + ((q * 32) << 16) + h * 64;
+        const uint32_t tl = tmem + ((q * 32) << 16) + a * NBUF * BN;
         uint32_t git = 0;
         for (uint32_t rb = blockIdx.x; rb < p.n_rb; rb += gridDim.x) {
             const uint32_t row = rb * BM + r;
             const bool valid = row < p.ma;
-            if (h == 0) { s_thr[r] = valid ? INF : -INF; s_cnt[r] = 0; }
+            float thr = valid ? INF : -INF;
+            uint32_t cnt = 0;
             for (uint32_t ti = 0; ti < p.n_ct; ti++, git++) {
                 const uint32_t t = tile_at(p, rb, ti);
                 const uint32_t buf = git % NBUF;
@@ -427,7 +431,9 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->tm_empty[buf]);   // accumulator now in registers
-                const uint32_t colh = t * BN + h * 64;
+                c0 = clock64();
+                pw[1] += c0 - c1;
+                const uint32_t col0 = t * BN;
                 if (p.noepi) {
                     if (v[0][lane] == 0x7fc00001u) p.out_ids[0] = v[1][lane];   // keep the loads live
                     continue;
@@ -436,34 +442,27 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     if (valid)
                         for (int ch = 0; ch < 2; ch++)
                             for (int j = 0; j < 32; j++)
-                                if (colh + ch * 32 + j < p.mb)
-                                    p.probe[(uint64_t)row * p.mb + colh + ch * 32 + j] = __uint_as_float(v[ch][j]);
+                                if (col0 + ch * 32 + j < p.mb)
+                                    p.probe[(uint64_t)row * p.mb + col0 + ch * 32 + j] = __uint_as_float(v[ch][j]);
                     continue;
                 }
-                named_bar_sync(1 + q, 64);               // both halves finished the previous tile
-                c0 = clock64();
-                pw[1] += c0 - c1;
-                // rows whose buffer cannot take this tile's <= 128 candidates are compacted
-                uint32_t need = __ballot_sync(0xffffffffu, s_cnt[r] > C - 128);
-                if (need) {
-                    uint32_t mine = need & (h ? 0xAAAAAAAAu : 0x55555555u);
-                    while (mine) {
-                        const int o = __ffs(mine) - 1;
-                        mine &= mine - 1;
-                        uint32_t kept;
-                        const uint32_t kth = select_L<EPL>(quadrows + (uint64_t)o * C, s_cnt[q * 32 + o], p.L, keep_max,
-                                                           hist, lane, &kept);
-                        if (lane == 0) { s_cnt[q * 32 + o] = kept; s_thr[q * 32 + o] = ord2f(kth); }
-                    }
-                    __syncwarp();
-                    named_bar_sync(1 + q, 64);
+                // reported ids of the tile's columns, fetched early (latency hidden by the masks)
+                const uint32_t id0 = p.col_map ? __ldg(p.col_map + col0 + lane) : col0 + lane;
+                const uint32_t id1 = p.col_map ? __ldg(p.col_map + col0 + 32 + lane) : col0 + 32 + lane;
+                // make room: rows whose buffer cannot take another BN candidates are compacted
+                uint32_t need = __ballot_sync(0xffffffffu, cnt > C - BN);
+                while (need) {
+                    const int o = __ffs(need) - 1;
+                    need &= need - 1;
+                    const uint32_t c_o = __shfl_sync(0xffffffffu, cnt, o);
+                    uint32_t kept;
+                    const uint32_t kth = select_L<EPL>(warprows + (uint64_t)o * C, c_o, p.L, keep_max, hist, lane, &kept);
+                    if (lane == (uint32_t)o) { cnt = kept; thr = ord2f(kth); }
                 }
                 c1 = clock64();
                 pw[2] += c1 - c0;   // compaction
-                // inclusive test: the row's columns reach the buffer out of id order (two halves,
-                // rotated sweep), so ties are resolved by the exact selection at the end
-                const float te = next_up(s_thr[r]);
-                // pass masks: bit j = sign(key_j - te) (key < te; NaN / equal -> 0)
+                // strict test when columns arrive in increasing id, inclusive with the rotated sweep
+                const float te = p.rotate ? next_up(thr) : thr;
                 uint32_t mk[2];
 #pragma unroll
                 for (int ch = 0; ch < 2; ch++) {
@@ -481,12 +480,17 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     }
                     mk[ch] = mq[0] | (mq[1] << 8) | (mq[2] << 16) | (mq[3] << 24);
                 }
-                if (p.self_exclude && t == rb && (q >> 1) == h) mk[q & 1] &= ~(1u << lane);   // self column
+                // self column: row r of block rb is column rb*BM + r
+                if (p.self_exclude && col0 <= row && row < col0 + BN) {
+                    const uint32_t sc = row - col0;
+                    if (sc < 32) mk[0] &= ~(1u << sc);
+                    else mk[1] &= ~(1u << (sc - 32));
+                }
                 c0 = clock64();
                 pw[3] += c0 - c1;   // masks
                 if (__any_sync(0xffffffffu, (mk[0] | mk[1]) != 0)) {
-                    const uint32_t np = __popc(mk[0]) + __popc(mk[1]);
-                    uint32_t slot = np ? atomicAdd(&s_cnt[r], np) : 0;
+                    sids[lane] = id0;
+                    sids[32 + lane] = id1;
 #pragma unroll
                     for (int ch = 0; ch < 2; ch++) {
                         uint32_t m = mk[ch];
@@ -498,13 +502,13 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                                                   __uint_as_float(v[ch][4 * j4 + 2]),
                                                   __uint_as_float(v[ch][4 * j4 + 3]));
                         __syncwarp();
-                        const uint32_t cb = colh + ch * 32;
+                        pw[6] += __popc(m);
                         while (m) {
+                            pw[7]++;
                             const uint32_t c = 31 - __clz(m);
                             m ^= 1u << c;
                             const uint32_t kb = __float_as_uint(skeys[lane * KSTRIDE + c]);
-                            const uint32_t id = p.col_map ? __ldg(p.col_map + cb + c) : cb + c;
-                            myrow[slot++] = ((uint64_t)kb << 32) | id;
+                            myrow[cnt++] = ((uint64_t)kb << 32) | sids[ch * 32 + c];
                         }
                         __syncwarp();
                     }
@@ -513,14 +517,13 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             }
             if (p.probe || p.noepi) continue;
             const long long f0 = clock64();
-            // ---- final: exact top-L of each row sorted by (dist, id); rows split between the halves
-            named_bar_sync(1 + q, 64);
-            for (uint32_t i = 0; i < 16; i++) {
-                const uint32_t rr = q * 32 + h * 16 + i;
-                const uint32_t row_o = rb * BM + rr;
+            // ---- final: exact top-L of each of the warp's rows, sorted by (dist, id)
+            __syncwarp();
+            for (uint32_t o = 0; o < 32; o++) {
+                uint32_t c_o = __shfl_sync(0xffffffffu, cnt, o);
+                const uint32_t row_o = rb * BM + a * MSUB + q * 32 + o;
                 if (row_o >= p.ma) continue;
-                uint64_t* b0 = cta_base + (uint64_t)rr * C;
-                uint32_t c_o = s_cnt[rr];
+                uint64_t* b0 = warprows + (uint64_t)o * C;
                 if (c_o > p.L) {
                     uint32_t kept;
                     select_L<EPL>(b0, c_o, p.L, p.L, hist, lane, &kept);
@@ -530,17 +533,16 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 finish_row(b0, c_o, b0, 0, p.L, sortbuf, p.norm_a[row_o], p.out_ids + orow * p.L,
                            p.out_d + orow * p.L, lane);
             }
-            named_bar_sync(1 + q, 64);
             pw[5] += clock64() - f0;   // final phase
         }
     }
     if (p.prof && lane == 0)
-        for (int i = 0; i < 6; i++) atomicAdd(p.prof + warp * 8 + i, (unsigned long long)pw[i]);
+        for (int i = 0; i < 8; i++) atomicAdd(p.prof + warp * 8 + i, (unsigned long long)pw[i]);
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(NBUF * BN));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u));
     }
 }
 
@@ -557,13 +559,14 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-// 2-D map over a rows x kdim operand; box = (box_bytes / esize) elements x 128 rows.
-sg_status make_map(CUtensorMap* m, const void* base, uint64_t rows, uint32_t kdim, uint32_t esize, uint32_t box_bytes) {
+// 2-D map over a rows x kdim operand; box = (box_bytes / esize) elements x box_rows rows.
+sg_status make_map(CUtensorMap* m, const void* base, uint64_t rows, uint32_t kdim, uint32_t esize, uint32_t box_bytes,
+                   uint32_t box_rows) {
     auto enc = get_encode();
     if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return SG_ERR_CUDA; }
     cuuint64_t dims[2] = {kdim, rows};
     cuuint64_t strides[1] = {(cuuint64_t)kdim * esize};
-    cuuint32_t box[2] = {box_bytes / esize, 128u};
+    cuuint32_t box[2] = {box_bytes / esize, box_rows};
     cuuint32_t es[2] = {1, 1};
     const CUtensorMapSwizzle sw = box_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B;
     CUresult r = enc(m, esize == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
@@ -574,19 +577,19 @@ sg_status make_map(CUtensorMap* m, const void* base, uint64_t rows, uint32_t kdi
 }
 
 uint32_t cand_cap(uint32_t L) {
-    uint32_t c = 256;   // > 128 + L: room for one tile of candidates above the kept set
+    uint32_t c = 256;   // > BN + L: room for one tile of candidates above the kept set
     while (c < 4 * L && c < 1024) c <<= 1;
     return c;
 }
 
 template <int KIND, int NKA, int MINI, int EPL>
 sg_status launch_t(const CUtensorMap* maps, KnnParams& p, cudaStream_t st) {
-    constexpr uint32_t A_BYTES = NKA * ATOM + (MINI ? 1024u * ((MINIB + 1023) / 1024) : 0u);
-    const size_t fixed = A_BYTES + sizeof(Bars) + 128 + 4 * BM * 4 + NEPI * SCRATCH + 1024 + 64;
+    constexpr uint32_t AHALF = NKA * ATOM + (MINI ? MINIB : 0u);
+    const size_t fixed = NACC * AHALF + sizeof(Bars) + 128 + NEPI * SCRATCH + 1024 + 64;
     const size_t budget = 227 * 1024;
+    if (fixed + (NKA + MINI) * SLOT > budget) { set_error("kNN: operand too wide for shared memory"); return SG_ERR_UNSUPPORTED; }
     uint32_t stages = (uint32_t)((budget - fixed) / SLOT);
     if (stages > MAX_STAGES) stages = MAX_STAGES;
-    if (stages < NKA + MINI) { set_error("kNN: operand too wide for shared memory"); return SG_ERR_UNSUPPORTED; }
     p.stages = stages;
     const size_t smem = fixed + stages * SLOT;
     auto kern = knn_tc_kernel<KIND, NKA, MINI, EPL>;
@@ -606,10 +609,8 @@ sg_status launch_nka(int nka, const CUtensorMap* maps, KnnParams& p, cudaStream_
         case 2: return launch_t<KIND, 2, MINI, EPL>(maps, p, st);
         case 3: return launch_t<KIND, 3, MINI, EPL>(maps, p, st);
         case 4: return launch_t<KIND, 4, MINI, EPL>(maps, p, st);
-        case 5: return launch_t<KIND, 5, MINI, EPL>(maps, p, st);
-        case 6: return launch_t<KIND, 6, MINI, EPL>(maps, p, st);
     }
-    set_error("kNN: unsupported operand width (%d atoms)", nka);
+    set_error("kNN: unsupported operand width (%d atoms; max 4 per 128-row half)", nka);
     return SG_ERR_UNSUPPORTED;
 }
 
@@ -623,8 +624,10 @@ sg_status launch_mini(int nka, int mini, const CUtensorMap* maps, KnnParams& p, 
 unsigned long long* g_knn_prof = nullptr;
 void set_knn_profile(unsigned long long* buf) { g_knn_prof = buf; }
 
+uint32_t knn_row_align() { return BM; }
+
 size_t knn_core_workspace(uint32_t L) {
-    return (size_t)num_sms() * 2 * BM * cand_cap(L) * sizeof(uint64_t) + 4096;
+    return (size_t)num_sms() * BM * cand_cap(L) * sizeof(uint64_t) + 4096;
 }
 
 sg_status knn_core(const Operand& A, const Operand& B, int /*metric*/, bool self_exclude, uint32_t L, uint32_t* ids,
@@ -634,10 +637,11 @@ sg_status knn_core(const Operand& A, const Operand& B, int /*metric*/, bool self
         set_error("kNN: operand layout mismatch");
         return SG_ERR_INVALID_ARG;
     }
+    if (A.rows_pad % BM || B.rows_pad % BN) { set_error("kNN: operand rows not padded"); return SG_ERR_INVALID_ARG; }
     KnnParams p{};
     p.norm_a = A.norm;
     p.C = cand_cap(L);
-    p.cand = cv.take<uint64_t>((size_t)num_sms() * 2 * BM * p.C);
+    p.cand = cv.take<uint64_t>((size_t)num_sms() * BM * p.C);
     if (!cv.ok()) { set_error("kNN: workspace too small"); return SG_ERR_WORKSPACE; }
     p.out_ids = ids;
     p.out_d = dists;
@@ -654,18 +658,18 @@ sg_status knn_core(const Operand& A, const Operand& B, int /*metric*/, bool self
     p.rotate = rotate ? 1 : 0;
     {
         static int tb = -1;
-        if (tb < 0) { const char* e = getenv("SG_TBACK"); tb = e ? atoi(e) : 4; }
+        if (tb < 0) { const char* e = getenv("SG_TBACK"); tb = e ? atoi(e) : 8; }
         p.t_back = (uint32_t)tb;
         static int ne = -1;
         if (ne < 0) { const char* e = getenv("SG_KNN_NOEPI"); ne = e ? atoi(e) : 0; }
-        p.noepi = ne;
+        p.noepi = ne && rotate;   // only the main (reordered) sweep; the order pass needs its result
     }
     CUtensorMap maps[4];
-    SG_TRY(make_map(&maps[0], A.a, A.rows_pad, A.kdim, A.esize, 128));
-    SG_TRY(make_map(&maps[1], B.b, B.rows_pad, B.kdim, B.esize, 128));
+    SG_TRY(make_map(&maps[0], A.a, A.rows_pad, A.kdim, A.esize, 128, MSUB));
+    SG_TRY(make_map(&maps[1], B.b, B.rows_pad, B.kdim, B.esize, 128, BN));
     if (A.mini) {
-        SG_TRY(make_map(&maps[2], A.a, A.rows_pad, A.kdim, A.esize, 32));
-        SG_TRY(make_map(&maps[3], B.b, B.rows_pad, B.kdim, B.esize, 32));
+        SG_TRY(make_map(&maps[2], A.a, A.rows_pad, A.kdim, A.esize, 32, MSUB));
+        SG_TRY(make_map(&maps[3], B.b, B.rows_pad, B.kdim, B.esize, 32, BN));
     } else {
         maps[2] = maps[0];
         maps[3] = maps[1];

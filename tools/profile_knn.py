@@ -45,11 +45,13 @@ def main():
         api.scalegann_knn(x, a.L, precision=a.precision, ws=ws)
         torch.cuda.synchronize()
         api.scalegann_knn_profile(None)
-        c = cnt.view(10, 8)[:, :6].double().cpu()
+        c = cnt.view(10, 8).double().cpu()
         names = ["wait", "tmem/full", "compact", "mask", "insert", "final"]
-        tot = c.sum(1, keepdim=True)
         for w in range(10):
-            print(f"warp {w}: " + " ".join(f"{n}={v / 1e9:.2f}G" for n, v in zip(names, c[w].tolist())))
+            print(f"warp {w}: " + " ".join(f"{n}={v / 1e9:.2f}G" for n, v in zip(names, c[w, :6].tolist())))
+        ins = c[2:, 6].sum().item() * 32 / 32   # lane-0 sums of its own row only
+        print(f"insertions (lane-0 rows) per row: {c[2:, 6].sum().item() / (8 * 148 * max(1, (a.m // 256) // 148)):.1f}"
+              f"  loop iterations per warp-row-block: {c[2:, 7].sum().item() / (8 * 148 * max(1, (a.m // 256) // 148)):.1f}")
     per = ms / max(nl, 1)
     fl = 2.0 * a.m * a.m * a.d
     print(json.dumps({"m": a.m, "d": a.d, "L": a.L, "ms_per_launch": per, "tflops": fl / (per / 1e3) / 1e12}))
