@@ -8,15 +8,15 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(HERE, "build", "obj")
-LIB = os.path.join(HERE, "libscalegann.so")
+OBJ = os.path.join(HERE, "build", os.environ.get("SG_OBJ_DIR", "obj"))
+LIB = os.environ.get("SG_LIB_PATH", os.path.join(HERE, "libscalegann.so"))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
     "-Xcompiler", "-fPIC",
     "-I", os.path.join(os.path.dirname(HERE), "include"),
-]
+] + os.environ.get("SG_NVCC_FLAGS", "").split()
 
 
 def _deps_mtime() -> float:

@@ -33,9 +33,15 @@ namespace sg {
 namespace {
 
 constexpr uint32_t MSUB = 128;           // rows per accumulator (MMA M)
-constexpr uint32_t NACC = 2;             // accumulators (row halves) per CTA
-constexpr uint32_t BM = MSUB * NACC;     // rows per CTA row block
-constexpr uint32_t BN = 64;              // columns per tile (MMA N)
+constexpr uint32_t NACC_MAX = 2;         // accumulators (row halves) per CTA: 2 (f16), 1 (tf32: wider A)
+constexpr uint32_t BM = MSUB * NACC_MAX; // rows per CTA row block (operand padding unit)
+#ifndef SG_BN
+#define SG_BN 128
+#endif
+#ifndef SG_ATM
+#define SG_ATM 0
+#endif
+constexpr uint32_t BN = SG_BN;           // columns per tile (MMA N); N=64 MMAs lose ~45% to issue overhead
 constexpr uint32_t ATOM = 128 * 128;     // A atom: 128 rows x 128 B (128B swizzle)
 constexpr uint32_t MINIB = 128 * 32;     // A mini atom: 128 rows x 32 B (32B swizzle)
 constexpr uint32_t BATOM = BN * 128;     // B atom: 64 rows x 128 B
@@ -44,7 +50,8 @@ constexpr uint32_t SLOT = BATOM;         // B ring slot
 constexpr uint32_t NEPI = 8;             // epilogue warps
 constexpr uint32_t NTHREADS = 64 + NEPI * 32;
 constexpr uint32_t MAX_STAGES = 32;
-constexpr uint32_t NBUF = 4;             // TMEM buffers per accumulator (2 x 4 x 64 = 512 columns)
+constexpr uint32_t NBUF_MAX = 4;         // TMEM buffers per accumulator: 4 (A in smem) or 2 (A in TMEM)
+constexpr uint32_t ACOL = 256;           // A in TMEM: half a at columns ACOL + 128 a
 constexpr uint32_t KSTRIDE = 36;         // floats per staged row (16B aligned, conflict-free)
 constexpr uint32_t SCRATCH = 32 * KSTRIDE * 4 + 64 * 4;   // per warp: staged keys | hist | sort buffer, + tile ids
 
@@ -113,6 +120,19 @@ __device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&v)[3
           "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
         : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
+                 "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// tcgen05.mma with A from tensor memory (TS)
+__device__ __forceinline__ void tc_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(acc));
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // Shared-memory matrix descriptors, K-major: 128B swizzle (8-row groups 1024 B apart) and
@@ -155,15 +175,19 @@ struct KnnParams {
     const uint32_t* row_map;   // A row (operand order) -> output row (nullptr = identity)
     const uint32_t* col_map;   // B row (operand order) -> reported id (nullptr = identity)
     uint32_t ma, mb, L, C, n_rb, n_ct, stages;
+    uint32_t rb_rows;          // rows per row block (128 * accumulators)
     uint32_t t_back;           // with rotate: a row block starts t_back tiles before its diagonal
     int rotate;                // column tiles visited from the diagonal - t_back cyclically
     int self_exclude;
     int noepi;                 // diagnostics: epilogue only drains TMEM (pipeline speed test)
+    int noload;                // diagnostics: producer skips the B loads (tensor-core speed test)
+    const uint4* a_glob;       // A side operand rows (for A-in-TMEM), kdim halves per row
+    uint32_t a_words;          // 32-bit words per A row
 };
 
 __device__ __forceinline__ uint32_t tile_at(const KnnParams& p, uint32_t rb, uint32_t i) {
     if (!p.rotate) return i;
-    const uint32_t diag = rb * (BM / BN) % p.n_ct;
+    const uint32_t diag = rb * (p.rb_rows / BN) % p.n_ct;
     const uint32_t back = p.t_back % p.n_ct;
     return (diag + p.n_ct - back + i) % p.n_ct;
 }
@@ -171,7 +195,7 @@ __device__ __forceinline__ uint32_t tile_at(const KnnParams& p, uint32_t rb, uin
 struct __align__(8) Bars {
     uint64_t full[MAX_STAGES], empty[MAX_STAGES];
     uint64_t a_full, a_empty;
-    uint64_t tm_full[NBUF], tm_empty[NBUF];
+    uint64_t tm_full[NBUF_MAX], tm_empty[NBUF_MAX];
     uint32_t tmem_base;
 };
 
@@ -185,7 +209,7 @@ __device__ __forceinline__ uint64_t ord2raw(uint64_t w) {
 }
 
 template <int EPL>
-__device__ uint32_t select_L(uint64_t* rb, uint32_t cnt, uint32_t L, uint32_t keep_max, uint32_t* hist,
+__device__ __forceinline__ uint32_t select_L(uint64_t* rb, uint32_t cnt, uint32_t L, uint32_t keep_max, uint32_t* hist,
                          uint32_t lane, uint32_t* kept) {
     uint64_t e[EPL];
 #pragma unroll
@@ -283,9 +307,15 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     constexpr uint32_t EL = KIND ? 4 : 2;                  // bytes per element
     constexpr uint32_t ATOM_K = 128 / EL;                  // elements per 128B atom
     constexpr uint32_t NSLOT = NKA + MINI;                 // ring slots per column tile
-    constexpr uint32_t AHALF = NKA * ATOM + (MINI ? MINIB : 0u);   // bytes of one 128-row half
+    // f16 operands: A lives in TMEM (read once per row block), so the tensor core streams only
+    // B from shared memory; tf32 (wider A) keeps A in shared memory.
+    constexpr uint32_t NACC = KIND == 0 ? NACC_MAX : 1;   // tf32 A halves do not both fit in smem
+    constexpr uint32_t RB = MSUB * NACC;                  // rows per row block of this instantiation
+    constexpr bool ATM = KIND == 0 && SG_ATM;
+    constexpr uint32_t NBUF = ATM ? 2 : 512 / (NACC * BN);
+    constexpr uint32_t AHALF = ATM ? 0u : NKA * ATOM + (MINI ? MINIB : 0u);   // smem bytes of one 128-row half
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint8_t* sA = smem;                                    // [NACC][NKA atoms + mini]
+    uint8_t* sA = smem;                                    // [NACC][NKA atoms + mini] (SS mode)
     uint8_t* sB = smem + NACC * AHALF;
     Bars* bars = (Bars*)(sB + p.stages * SLOT);
     uint8_t* scratch_all = (uint8_t*)(((uintptr_t)(bars + 1) + 127) & ~(uintptr_t)127);   // NEPI x SCRATCH
@@ -295,9 +325,9 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
 
     if (threadIdx.x == 0) {
         for (uint32_t s = 0; s < p.stages; s++) { mbar_init(&bars->full[s], 1); mbar_init(&bars->empty[s], 1); }
-        mbar_init(&bars->a_full, 1);
+        mbar_init(&bars->a_full, ATM ? 4 * NACC : 1);
         mbar_init(&bars->a_empty, 1);
-        for (uint32_t b = 0; b < NBUF; b++) { mbar_init(&bars->tm_full[b], 1); mbar_init(&bars->tm_empty[b], NEPI); }
+        for (uint32_t b = 0; b < NBUF_MAX; b++) { mbar_init(&bars->tm_full[b], 1); mbar_init(&bars->tm_empty[b], 4 * NACC); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -324,13 +354,15 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         if (lane == 0) {
             uint32_t stage = 0, sph = 0, it = 0;
             for (uint32_t rb = blockIdx.x; rb < p.n_rb; rb += gridDim.x, it++) {
-                if (it > 0) mbar_wait(&bars->a_empty, (it - 1) & 1);
-                mbar_expect_tx(&bars->a_full, NACC * AHALF);
-                for (uint32_t a = 0; a < NACC; a++) {
+                if (!ATM) {
+                    if (it > 0) mbar_wait(&bars->a_empty, (it - 1) & 1);
+                    mbar_expect_tx(&bars->a_full, NACC * AHALF);
+                }
+                for (uint32_t a = 0; a < NACC && !ATM; a++) {
                     uint8_t* base = sA + a * AHALF;
                     for (int ka = 0; ka < NKA; ka++)
-                        tma_load_2d(&tmA, &bars->a_full, base + ka * ATOM, ka * ATOM_K, rb * BM + a * MSUB);
-                    if (MINI) tma_load_2d(&tmAm, &bars->a_full, base + NKA * ATOM, NKA * ATOM_K, rb * BM + a * MSUB);
+                        tma_load_2d(&tmA, &bars->a_full, base + ka * ATOM, ka * ATOM_K, rb * RB + a * MSUB);
+                    if (MINI) tma_load_2d(&tmAm, &bars->a_full, base + NKA * ATOM, NKA * ATOM_K, rb * RB + a * MSUB);
                 }
                 for (uint32_t ti = 0; ti < p.n_ct; ti++) {
                     const uint32_t t = tile_at(p, rb, ti);
@@ -338,7 +370,9 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
 #pragma unroll
                     for (uint32_t ka = 0; ka < NSLOT; ka++) {
                         mbar_wait(&bars->empty[stage], sph ^ 1);
-                        if (ka < NKA) {
+                        if (p.noload) {
+                            mbar_arrive(&bars->full[stage]);
+                        } else if (ka < NKA) {
                             mbar_expect_tx(&bars->full[stage], BATOM);
                             tma_load_2d(&tmB, &bars->full[stage], sB + stage * SLOT, ka * ATOM_K, t * BN);
                         } else {
@@ -377,13 +411,25 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                         for (uint32_t a = 0; a < NACC; a++) {
                             const uint32_t dcol = tmem + (a * NBUF + buf) * BN;
                             const uint32_t abase = a_base + a * AHALF;
-                            if (ka < NKA) {
+                            if constexpr (ATM) {
+                                const uint32_t at = tmem + ACOL + a * 128;   // 8 columns per K step of 16
+                                if (ka < NKA) {
 #pragma unroll
-                                for (uint32_t kk = 0; kk < 4; kk++)
-                                    tc_mma<KIND>(dcol, desc_sw128(abase + ka * ATOM + kk * 32), desc_sw128(bslot + kk * 32),
-                                                 idesc, (ka | kk) != 0);
+                                    for (uint32_t kk = 0; kk < 4; kk++)
+                                        tc_mma_ts(dcol, at + (ka * 4 + kk) * 8, desc_sw128(bslot + kk * 32), idesc,
+                                                  (ka | kk) != 0);
+                                } else {
+                                    tc_mma_ts(dcol, at + NKA * 32, desc_sw32(bslot), idesc, NKA != 0);
+                                }
                             } else {
-                                tc_mma<KIND>(dcol, desc_sw32(abase + NKA * ATOM), desc_sw32(bslot), idesc, NKA != 0);
+                                if (ka < NKA) {
+#pragma unroll
+                                    for (uint32_t kk = 0; kk < 4; kk++)
+                                        tc_mma<KIND>(dcol, desc_sw128(abase + ka * ATOM + kk * 32),
+                                                     desc_sw128(bslot + kk * 32), idesc, (ka | kk) != 0);
+                                } else {
+                                    tc_mma<KIND>(dcol, desc_sw32(abase + NKA * ATOM), desc_sw32(bslot), idesc, NKA != 0);
+                                }
                             }
                         }
                         tc_commit(&bars->empty[stage]);
@@ -391,7 +437,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     }
                     tc_commit(&bars->tm_full[buf]);
                 }
-                tc_commit(&bars->a_empty);
+                if (!ATM) tc_commit(&bars->a_empty);
             }
         }
     } else {
@@ -404,17 +450,32 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         uint64_t* sortbuf = (uint64_t*)scratch;              // 512 (aliases skeys)
         uint32_t* sids = (uint32_t*)(scratch + 32 * KSTRIDE * 4);   // 64 reported ids of the tile
         const uint32_t C = p.C;
-        const uint32_t keep_max = p.L + (C - BN - p.L) / 4;  // approximate in-loop compaction target
+        const uint32_t keep_max = p.L + (C - 32 - p.L) / 4;  // approximate in-loop compaction target
         uint64_t* myrow = p.cand + ((uint64_t)blockIdx.x * BM + r) * C;
         uint64_t* warprows = p.cand + ((uint64_t)blockIdx.x * BM + a * MSUB + q * 32) * C;
         const float INF = __int_as_float(0x7f800000);
         const uint32_t tl = tmem + ((q * 32) << 16) + a * NBUF * BN;
         uint32_t git = 0;
-        for (uint32_t rb = blockIdx.x; rb < p.n_rb; rb += gridDim.x) {
-            const uint32_t row = rb * BM + r;
+        for (uint32_t rb = blockIdx.x; rb < p.n_rb && a < NACC; rb += gridDim.x) {
+            const uint32_t row = rb * RB + r;
             const bool valid = row < p.ma;
             float thr = valid ? INF : -INF;
             uint32_t cnt = 0;
+            if constexpr (ATM) {
+                // this row's A operand into TMEM (lane = row, K packed 2 per column); all MMAs of
+                // the previous row block completed before its last tile reached this warp
+                const uint4* src = p.a_glob + (uint64_t)row * (p.a_words / 4);
+                const uint32_t ta = tmem + ((q * 32) << 16) + ACOL + a * 128;
+                for (uint32_t c = 0; c < p.a_words; c += 8) {
+                    const uint4 u0 = __ldg(src + c / 4), u1 = __ldg(src + c / 4 + 1);
+                    const uint32_t w8[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+                    tmem_st8(ta + c, w8);
+                }
+                tmem_wait_st();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->a_full);
+            }
             for (uint32_t ti = 0; ti < p.n_ct; ti++, git++) {
                 const uint32_t t = tile_at(p, rb, ti);
                 const uint32_t buf = git % NBUF;
@@ -424,48 +485,57 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 pw[0] += c1 - c0;
                 tc_fence_after();
                 const uint32_t tb = tl + buf * BN;
-                uint32_t v[2][32];
-                tmem_ld32_nowait(tb, v[0]);
-                tmem_ld32_nowait(tb + 32, v[1]);
-                tmem_wait_ld();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&bars->tm_empty[buf]);   // accumulator now in registers
-                c0 = clock64();
-                pw[1] += c0 - c1;
-                const uint32_t col0 = t * BN;
-                if (p.noepi) {
-                    if (v[0][lane] == 0x7fc00001u) p.out_ids[0] = v[1][lane];   // keep the loads live
-                    continue;
-                }
-                if (p.probe) {
-                    if (valid)
-                        for (int ch = 0; ch < 2; ch++)
-                            for (int j = 0; j < 32; j++)
-                                if (col0 + ch * 32 + j < p.mb)
-                                    p.probe[(uint64_t)row * p.mb + col0 + ch * 32 + j] = __uint_as_float(v[ch][j]);
-                    continue;
-                }
-                // reported ids of the tile's columns, fetched early (latency hidden by the masks)
-                const uint32_t id0 = p.col_map ? __ldg(p.col_map + col0 + lane) : col0 + lane;
-                const uint32_t id1 = p.col_map ? __ldg(p.col_map + col0 + 32 + lane) : col0 + 32 + lane;
-                // make room: rows whose buffer cannot take another BN candidates are compacted
-                uint32_t need = __ballot_sync(0xffffffffu, cnt > C - BN);
-                while (need) {
-                    const int o = __ffs(need) - 1;
-                    need &= need - 1;
-                    const uint32_t c_o = __shfl_sync(0xffffffffu, cnt, o);
-                    uint32_t kept;
-                    const uint32_t kth = select_L<EPL>(warprows + (uint64_t)o * C, c_o, p.L, keep_max, hist, lane, &kept);
-                    if (lane == (uint32_t)o) { cnt = kept; thr = ord2f(kth); }
-                }
-                c1 = clock64();
-                pw[2] += c1 - c0;   // compaction
-                // strict test when columns arrive in increasing id, inclusive with the rotated sweep
-                const float te = p.rotate ? next_up(thr) : thr;
-                uint32_t mk[2];
+#pragma unroll 1
+                for (uint32_t hp = 0; hp < BN / 32; hp++) {
+                    // 32 columns of the tile per pass (register budget: 10 warps x 168 registers);
+                    // the accumulator buffer is released once the last pass is in registers
+                    uint32_t v[32];
+                    if (p.noepi >= 3) {
 #pragma unroll
-                for (int ch = 0; ch < 2; ch++) {
+                        for (int j = 0; j < 32; j++) v[j] = 0;
+                    } else {
+                        tmem_ld32_nowait(tb + hp * 32, v);
+                    }
+                    tmem_wait_ld();
+                    if (hp == BN / 32 - 1) {
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&bars->tm_empty[buf]);
+                    }
+                    c0 = clock64();
+                    pw[1] += c0 - c1;
+                    const uint32_t col0 = t * BN + hp * 32;
+                    if (p.noepi) {
+                        if ((v[0] ^ v[31]) == 0x7fc00001u) p.out_ids[0] = v[1];   // keep the loads live
+                        c1 = clock64();
+                        continue;
+                    }
+                    if (p.probe) {
+                        if (valid) {
+#pragma unroll
+                            for (int j = 0; j < 32; j++)
+                                if (col0 + j < p.mb) p.probe[(uint64_t)row * p.mb + col0 + j] = __uint_as_float(v[j]);
+                        }
+                        c1 = clock64();
+                        continue;
+                    }
+                    // reported id of this lane's column, fetched early (latency hidden by the mask)
+                    const uint32_t id0 = p.col_map ? __ldg(p.col_map + col0 + lane) : col0 + lane;
+                    // make room: rows whose buffer cannot take another 32 candidates are compacted
+                    uint32_t need = __ballot_sync(0xffffffffu, cnt > C - 32);
+                    while (need) {
+                        const int o = __ffs(need) - 1;
+                        need &= need - 1;
+                        const uint32_t c_o = __shfl_sync(0xffffffffu, cnt, o);
+                        uint32_t kept;
+                        const uint32_t kth =
+                            select_L<EPL>(warprows + (uint64_t)o * C, c_o, p.L, keep_max, hist, lane, &kept);
+                        if (lane == (uint32_t)o) { cnt = kept; thr = ord2f(kth); }
+                    }
+                    c1 = clock64();
+                    pw[2] += c1 - c0;   // compaction
+                    // strict test when columns arrive in increasing id, inclusive with the rotated sweep
+                    const float te = p.rotate ? next_up(thr) : thr;
                     uint32_t mq[4] = {0, 0, 0, 0};
 #pragma unroll
                     for (int s = 7; s >= 1; s -= 2) {
@@ -473,34 +543,23 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                         for (int g = 0; g < 4; g++) {
                             const int j = g * 8 + s;
                             uint32_t lo, hi;
-                            sub2(v[ch][j - 1], v[ch][j], te, lo, hi);
+                            sub2(v[j - 1], v[j], te, lo, hi);
                             mq[g] = __funnelshift_l(hi, mq[g], 1);
                             mq[g] = __funnelshift_l(lo, mq[g], 1);
                         }
                     }
-                    mk[ch] = mq[0] | (mq[1] << 8) | (mq[2] << 16) | (mq[3] << 24);
-                }
-                // self column: row r of block rb is column rb*BM + r
-                if (p.self_exclude && col0 <= row && row < col0 + BN) {
-                    const uint32_t sc = row - col0;
-                    if (sc < 32) mk[0] &= ~(1u << sc);
-                    else mk[1] &= ~(1u << (sc - 32));
-                }
-                c0 = clock64();
-                pw[3] += c0 - c1;   // masks
-                if (__any_sync(0xffffffffu, (mk[0] | mk[1]) != 0)) {
-                    sids[lane] = id0;
-                    sids[32 + lane] = id1;
-#pragma unroll
-                    for (int ch = 0; ch < 2; ch++) {
-                        uint32_t m = mk[ch];
-                        if (!__any_sync(0xffffffffu, m != 0)) continue;
+                    uint32_t m = mq[0] | (mq[1] << 8) | (mq[2] << 16) | (mq[3] << 24);
+                    // self column: row r of block rb is column rb*RB + r
+                    if (p.self_exclude && col0 <= row && row < col0 + 32) m &= ~(1u << (row - col0));
+                    c0 = clock64();
+                    pw[3] += c0 - c1;   // masks
+                    if (__any_sync(0xffffffffu, m != 0)) {
+                        sids[lane] = id0;
                         float4* st4 = (float4*)(skeys + lane * KSTRIDE);
 #pragma unroll
                         for (int j4 = 0; j4 < 8; j4++)
-                            st4[j4] = make_float4(__uint_as_float(v[ch][4 * j4]), __uint_as_float(v[ch][4 * j4 + 1]),
-                                                  __uint_as_float(v[ch][4 * j4 + 2]),
-                                                  __uint_as_float(v[ch][4 * j4 + 3]));
+                            st4[j4] = make_float4(__uint_as_float(v[4 * j4]), __uint_as_float(v[4 * j4 + 1]),
+                                                  __uint_as_float(v[4 * j4 + 2]), __uint_as_float(v[4 * j4 + 3]));
                         __syncwarp();
                         pw[6] += __popc(m);
                         while (m) {
@@ -508,12 +567,13 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                             const uint32_t c = 31 - __clz(m);
                             m ^= 1u << c;
                             const uint32_t kb = __float_as_uint(skeys[lane * KSTRIDE + c]);
-                            myrow[cnt++] = ((uint64_t)kb << 32) | sids[ch * 32 + c];
+                            myrow[cnt++] = ((uint64_t)kb << 32) | sids[c];
                         }
                         __syncwarp();
                     }
+                    c1 = clock64();
+                    pw[4] += c1 - c0;   // insertions
                 }
-                pw[4] += clock64() - c0;   // insertions
             }
             if (p.probe || p.noepi) continue;
             const long long f0 = clock64();
@@ -521,7 +581,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             __syncwarp();
             for (uint32_t o = 0; o < 32; o++) {
                 uint32_t c_o = __shfl_sync(0xffffffffu, cnt, o);
-                const uint32_t row_o = rb * BM + a * MSUB + q * 32 + o;
+                const uint32_t row_o = rb * RB + a * MSUB + q * 32 + o;
                 if (row_o >= p.ma) continue;
                 uint64_t* b0 = warprows + (uint64_t)o * C;
                 if (c_o > p.L) {
@@ -584,7 +644,8 @@ uint32_t cand_cap(uint32_t L) {
 
 template <int KIND, int NKA, int MINI, int EPL>
 sg_status launch_t(const CUtensorMap* maps, KnnParams& p, cudaStream_t st) {
-    constexpr uint32_t AHALF = NKA * ATOM + (MINI ? MINIB : 0u);
+    constexpr uint32_t AHALF = (KIND == 0 && SG_ATM) ? 0u : NKA * ATOM + (MINI ? MINIB : 0u);   // A in TMEM for f16
+    constexpr uint32_t NACC = KIND == 0 ? NACC_MAX : 1;
     const size_t fixed = NACC * AHALF + sizeof(Bars) + 128 + NEPI * SCRATCH + 1024 + 64;
     const size_t budget = 227 * 1024;
     if (fixed + (NKA + MINI) * SLOT > budget) { set_error("kNN: operand too wide for shared memory"); return SG_ERR_UNSUPPORTED; }
@@ -640,6 +701,8 @@ sg_status knn_core(const Operand& A, const Operand& B, int /*metric*/, bool self
     if (A.rows_pad % BM || B.rows_pad % BN) { set_error("kNN: operand rows not padded"); return SG_ERR_INVALID_ARG; }
     KnnParams p{};
     p.norm_a = A.norm;
+    p.a_glob = (const uint4*)A.a;
+    p.a_words = A.kdim * A.esize / 4;
     p.C = cand_cap(L);
     p.cand = cv.take<uint64_t>((size_t)num_sms() * BM * p.C);
     if (!cv.ok()) { set_error("kNN: workspace too small"); return SG_ERR_WORKSPACE; }
@@ -650,7 +713,8 @@ sg_status knn_core(const Operand& A, const Operand& B, int /*metric*/, bool self
     p.ma = (uint32_t)A.rows;
     p.mb = (uint32_t)B.rows;
     p.L = L;
-    p.n_rb = (uint32_t)(A.rows_pad / BM);
+    p.rb_rows = MSUB * (A.esize == 2 ? NACC_MAX : 1);
+    p.n_rb = (uint32_t)(A.rows_pad / p.rb_rows);
     p.n_ct = (uint32_t)(B.rows_pad / BN);
     p.self_exclude = self_exclude ? 1 : 0;
     p.row_map = row_map;
@@ -663,6 +727,9 @@ sg_status knn_core(const Operand& A, const Operand& B, int /*metric*/, bool self
         static int ne = -1;
         if (ne < 0) { const char* e = getenv("SG_KNN_NOEPI"); ne = e ? atoi(e) : 0; }
         p.noepi = ne && rotate;   // only the main (reordered) sweep; the order pass needs its result
+        static int nl = -1;
+        if (nl < 0) { const char* e = getenv("SG_KNN_NOLOAD"); nl = e ? atoi(e) : 0; }
+        p.noload = nl && rotate && ne;
     }
     CUtensorMap maps[4];
     SG_TRY(make_map(&maps[0], A.a, A.rows_pad, A.kdim, A.esize, 128, MSUB));
