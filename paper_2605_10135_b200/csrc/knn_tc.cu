@@ -181,6 +181,7 @@ struct KnnParams {
     int self_exclude;
     int noepi;                 // diagnostics: epilogue only drains TMEM (pipeline speed test)
     int noload;                // diagnostics: producer skips the B loads (tensor-core speed test)
+    int abl;                   // diagnostics ablation bits: 1 no insertion, 2 no id fetch, 4 no clock64
     const uint4* a_glob;       // A side operand rows (for A-in-TMEM), kdim halves per row
     uint32_t a_words;          // 32-bit words per A row
 };
@@ -208,25 +209,58 @@ __device__ __forceinline__ uint64_t ord2raw(uint64_t w) {
     return ((uint64_t)__float_as_uint(ord2f((uint32_t)(w >> 32))) << 32) | (uint32_t)w;
 }
 
+__device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t t = __shfl_xor_sync(0xffffffffu, v, o);
+        v = t < v ? t : v;
+    }
+    return v;
+}
+__device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t t = __shfl_xor_sync(0xffffffffu, v, o);
+        v = t > v ? t : v;
+    }
+    return v;
+}
+
+// Warp-cooperative radix selection over rb[0..cnt) (cnt > L).  Keeps, in place at rb[0..kept), a
+// prefix of the (key, id) order with L <= kept <= keep_max (keep_max = L: exactly the L smallest)
+// and returns the largest kept key (ordered u32).  8-bit digits start at the highest bit where the
+// smallest and largest candidate differ (the shared prefix would put every candidate in one
+// histogram bin), counted with shared-memory atomics.  All 32 lanes call with the same arguments.
 template <int EPL>
-__device__ __forceinline__ uint32_t select_L(uint64_t* rb, uint32_t cnt, uint32_t L, uint32_t keep_max, uint32_t* hist,
-                         uint32_t lane, uint32_t* kept) {
+__device__ __forceinline__ uint32_t select_L(uint64_t* rb, uint32_t cnt, uint32_t L, uint32_t keep_max,
+                                             uint32_t* hist, uint32_t lane, uint32_t* kept) {
     uint64_t e[EPL];
+    uint64_t lo = ~0ull, hi = 0;
 #pragma unroll
     for (int i = 0; i < EPL; i++) {
         const uint32_t idx = i * 32 + lane;
         e[i] = idx < cnt ? raw2ord(rb[idx]) : ~0ull;
+        if (idx < cnt) { lo = e[i] < lo ? e[i] : lo; hi = e[i] > hi ? e[i] : hi; }
     }
-    uint64_t pfx = 0;
-    uint32_t want = L, cut = 0;
+    lo = warp_min_u64(lo);
+    hi = warp_max_u64(hi);
+    // bits [top, 64) are common to every candidate
+    int top = 64 - __clzll(lo ^ hi);              // 0 only if all equal (cannot happen: ids differ)
+    uint64_t pfx = top >= 64 ? 0ull : (lo >> top) << top;
+    uint32_t want = L;
+    int cut = top;
+    uint32_t kp = 0;
 #pragma unroll 1
-    for (int sh = 56; sh >= 0; sh -= 8) {
+    while (top > 0) {
+        const int w = top >= 8 ? 8 : top;          // digit = bits [top - w, top)
+        const int sh = top - w;
         for (int b = lane; b < 256; b += 32) hist[b] = 0;
         __syncwarp();
-        const uint64_t hm = sh == 56 ? 0ull : (~0ull << (sh + 8));
+        const uint64_t hm = top >= 64 ? 0ull : (~0ull << top);
+        const uint32_t dmask = (1u << w) - 1u;
 #pragma unroll
         for (int i = 0; i < EPL; i++)
-            if ((e[i] & hm) == (pfx & hm)) atomicAdd(&hist[(uint32_t)(e[i] >> sh) & 255u], 1u);
+            if (e[i] != ~0ull && (e[i] & hm) == (pfx & hm)) atomicAdd(&hist[(uint32_t)(e[i] >> sh) & dmask], 1u);
         __syncwarp();
         uint32_t hv[8], loc = 0;
 #pragma unroll
@@ -250,15 +284,17 @@ __device__ __forceinline__ uint32_t select_L(uint64_t* rb, uint32_t cnt, uint32_
         want -= before;
         pfx |= (uint64_t)dg << sh;
         __syncwarp();
-        if (L - want + bc <= keep_max) { cut = sh; *kept = L - want + bc; break; }
+        top = sh;
+        // entries strictly below the chosen bucket: L - want; cutting here keeps the bucket too
+        if (L - want + bc <= keep_max || top == 0) { cut = sh; kp = L - want + bc; break; }
     }
-    const uint64_t lim = pfx >> cut;
+    const uint64_t lim = cut >= 64 ? ~0ull : pfx >> cut;
     uint32_t base = 0, mk = 0;
     __syncwarp();
 #pragma unroll
     for (int i = 0; i < EPL; i++) {
         const uint32_t idx = i * 32 + lane;
-        const bool s = idx < cnt && (e[i] >> cut) <= lim;
+        const bool s = idx < cnt && (cut >= 64 || (e[i] >> cut) <= lim);
         const uint32_t bal = __ballot_sync(0xffffffffu, s);
         if (s) {
             rb[base + __popc(bal & ((1u << lane) - 1u))] = ord2raw(e[i]);
@@ -269,6 +305,8 @@ __device__ __forceinline__ uint32_t select_L(uint64_t* rb, uint32_t cnt, uint32_
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mk = max(mk, __shfl_xor_sync(0xffffffffu, mk, o));
     __syncwarp();
+    *kept = base;
+    (void)kp;
     return mk;
 }
 
@@ -450,7 +488,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         uint64_t* sortbuf = (uint64_t*)scratch;              // 512 (aliases skeys)
         uint32_t* sids = (uint32_t*)(scratch + 32 * KSTRIDE * 4);   // 64 reported ids of the tile
         const uint32_t C = p.C;
-        const uint32_t keep_max = p.L + (C - 32 - p.L) / 4;  // approximate in-loop compaction target
+        const uint32_t keep_max = p.L + (C - 32 - p.L) / 8;  // approximate in-loop compaction target
         uint64_t* myrow = p.cand + ((uint64_t)blockIdx.x * BM + r) * C;
         uint64_t* warprows = p.cand + ((uint64_t)blockIdx.x * BM + a * MSUB + q * 32) * C;
         const float INF = __int_as_float(0x7f800000);
@@ -520,7 +558,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                         continue;
                     }
                     // reported id of this lane's column, fetched early (latency hidden by the mask)
-                    const uint32_t id0 = p.col_map ? __ldg(p.col_map + col0 + lane) : col0 + lane;
+                    const uint32_t id0 = (p.col_map && !(p.abl & 2)) ? __ldg(p.col_map + col0 + lane) : col0 + lane;
                     // make room: rows whose buffer cannot take another 32 candidates are compacted
                     uint32_t need = __ballot_sync(0xffffffffu, cnt > C - 32);
                     while (need) {
@@ -553,6 +591,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     if (p.self_exclude && col0 <= row && row < col0 + 32) m &= ~(1u << (row - col0));
                     c0 = clock64();
                     pw[3] += c0 - c1;   // masks
+                    if (p.abl & 1) m = 0;
                     if (__any_sync(0xffffffffu, m != 0)) {
                         sids[lane] = id0;
                         float4* st4 = (float4*)(skeys + lane * KSTRIDE);
@@ -730,6 +769,9 @@ sg_status knn_core(const Operand& A, const Operand& B, int /*metric*/, bool self
         static int nl = -1;
         if (nl < 0) { const char* e = getenv("SG_KNN_NOLOAD"); nl = e ? atoi(e) : 0; }
         p.noload = nl && rotate && ne;
+        static int ab = -1;
+        if (ab < 0) { const char* e = getenv("SG_KNN_ABL"); ab = e ? atoi(e) : 0; }
+        p.abl = rotate ? ab : 0;
     }
     CUtensorMap maps[4];
     SG_TRY(make_map(&maps[0], A.a, A.rows_pad, A.kdim, A.esize, 128, MSUB));

@@ -52,7 +52,7 @@ def main():
         ins = c[2:, 6].sum().item() * 32 / 32   # lane-0 sums of its own row only
         print(f"insertions (lane-0 rows) per row: {c[2:, 6].sum().item() / (8 * 148 * max(1, (a.m // 256) // 148)):.1f}"
               f"  loop iterations per warp-row-block: {c[2:, 7].sum().item() / (8 * 148 * max(1, (a.m // 256) // 148)):.1f}")
-    per = ms / max(nl, 1)
+    per = ms / a.reps   # per call (spatial-order pass + main sweep)
     fl = 2.0 * a.m * a.m * a.d
     print(json.dumps({"m": a.m, "d": a.d, "L": a.L, "ms_per_launch": per, "tflops": fl / (per / 1e3) / 1e12}))
 
