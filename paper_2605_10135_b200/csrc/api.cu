@@ -95,7 +95,7 @@ static uint32_t knn_full_atoms(int prec, int metric, uint32_t d) {
 static size_t knn_total_ws(uint64_t ma, uint64_t mb, uint32_t d, int prec, uint32_t L, bool same) {
     size_t b = same ? operand_bytes(prec, SG_L2, d, ma, SIDE_A | SIDE_B)
                     : operand_bytes(prec, SG_L2, d, ma, SIDE_A) + operand_bytes(prec, SG_L2, d, mb, SIDE_B);
-    return b + knn_core_workspace(L) + 2 * (ma * 4 + 256) + (same ? order_workspace(ma, d, prec, SG_L2) : 0) + 4096;
+    return b + knn_core_workspace(L, ma, d, prec, SG_L2) + 2 * (ma * 4 + 256) + (same ? order_workspace(ma, d, prec, SG_L2) : 0) + 4096;
 }
 
 static int worst_prec(sg_dtype dtype, int32_t precision) {
@@ -293,7 +293,7 @@ static size_t build_ws(uint64_t m, uint32_t d, sg_dtype dtype, const sg_build_pa
     size_t b = 1024;
     b += 2 * (m * p->L * 4 + 256);     // kNN ids + dists (when not caller-provided)
     b += 2 * (m * p->R * 4 + 256);     // pruned ids + dists
-    size_t knn = 2 * (m * 4 + 256) + operand_bytes(prec, p->metric, d, m, SIDE_A | SIDE_B) + knn_core_workspace(p->L) +
+    size_t knn = 2 * (m * 4 + 256) + operand_bytes(prec, p->metric, d, m, SIDE_A | SIDE_B) + knn_core_workspace(p->L, m, d, prec, p->metric) +
                  order_workspace(m, d, prec, p->metric) + 1024;
     size_t rev = reverse_ws(m, p->R);
     return b + (knn > rev ? knn : rev);

@@ -193,14 +193,14 @@ size_t operand_bytes(int prec, int metric, uint32_t d, uint64_t rows, int sides)
 sg_status gather_operand(const void* x, sg_dtype dtype, uint32_t d, const uint32_t* ids, uint64_t m,
                          int prec, int metric, int sides, Carver& cv, Operand* op, cudaStream_t st);
 // knn_tc.cu
-size_t knn_core_workspace(uint32_t L);
+size_t knn_core_workspace(uint32_t L, uint64_t ma, uint32_t d, int prec, int metric);
 // row_map / col_map translate operand order to output rows / reported ids (spatially
 // reordered shards); rotate visits column tiles starting just before the diagonal.
 sg_status knn_core(const Operand& A, const Operand& B, int metric, bool self_exclude, uint32_t L,
                    uint32_t* ids, float* dists, float* probe, Carver& cv, cudaStream_t st,
                    const uint32_t* row_map = nullptr, const uint32_t* col_map = nullptr, bool rotate = false);
 // order.cu: spatial order of a shard (rows grouped by nearest sub-centroid)
-uint32_t order_groups(uint64_t m);   // >= 2 when a spatial order is worth computing
+uint32_t order_groups(uint64_t m);   // >= 2 when the spatial order is enabled (SG_KNN_ORDER=1) and worth computing
 size_t order_workspace(uint64_t m, uint32_t d, int prec, int metric);
 sg_status spatial_order(const void* x, sg_dtype dtype, uint32_t d, const uint32_t* idmap, uint64_t m, int prec,
                         int metric, uint32_t* perm, uint32_t* ids_perm, Carver cv, cudaStream_t st);

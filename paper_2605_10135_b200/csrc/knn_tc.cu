@@ -23,318 +23,10 @@
 //           resident).  When a buffer nears full, the warp radix-selects (8-bit digits, smem
 //           histogram) a small superset of the L best and lowers the threshold; at the end of a
 //           row block the exact top-L is selected and sorted by (dist, id).
-#include <cuda.h>
-#include <cudaTypedefs.h>
-#include <stdlib.h>
-
-#include "common.cuh"
+#include "knn_common.cuh"
 
 namespace sg {
 namespace {
-
-constexpr uint32_t MSUB = 128;           // rows per accumulator (MMA M)
-constexpr uint32_t NACC_MAX = 2;         // accumulators (row halves) per CTA: 2 (f16), 1 (tf32: wider A)
-constexpr uint32_t BM = MSUB * NACC_MAX; // rows per CTA row block (operand padding unit)
-#ifndef SG_BN
-#define SG_BN 128
-#endif
-#ifndef SG_ATM
-#define SG_ATM 0
-#endif
-constexpr uint32_t BN = SG_BN;           // columns per tile (MMA N); N=64 MMAs lose ~45% to issue overhead
-constexpr uint32_t ATOM = 128 * 128;     // A atom: 128 rows x 128 B (128B swizzle)
-constexpr uint32_t MINIB = 128 * 32;     // A mini atom: 128 rows x 32 B (32B swizzle)
-constexpr uint32_t BATOM = BN * 128;     // B atom: 64 rows x 128 B
-constexpr uint32_t BMINI = BN * 32;      // B mini atom: 64 rows x 32 B
-constexpr uint32_t SLOT = BATOM;         // B ring slot
-constexpr uint32_t NEPI = 8;             // epilogue warps
-constexpr uint32_t NTHREADS = 64 + NEPI * 32;
-constexpr uint32_t MAX_STAGES = 32;
-constexpr uint32_t NBUF_MAX = 4;         // TMEM buffers per accumulator: 4 (A in smem) or 2 (A in TMEM)
-constexpr uint32_t ACOL = 256;           // A in TMEM: half a at columns ACOL + 128 a
-constexpr uint32_t KSTRIDE = 36;         // floats per staged row (16B aligned, conflict-free)
-constexpr uint32_t SCRATCH = 32 * KSTRIDE * 4 + 64 * 4;   // per warp: staged keys | hist | sort buffer, + tile ids
-
-// ----------------------------------------------------------------- PTX wrappers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-    uint32_t ok = 0;
-    const uint32_t a = smem_u32(b);
-    while (!ok) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(ok)
-            : "r"(a), "r"(parity)
-            : "memory");
-    }
-}
-__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-            smem_u32(dst)),
-        "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-                 : "memory");
-}
-template <int KIND>
-__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
-    if constexpr (KIND == 0) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
-    } else {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
-    }
-}
-__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&v)[32]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-          "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
-          "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
-          "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-        : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
-                 "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
-                 : "memory");
-}
-__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-// tcgen05.mma with A from tensor memory (TS)
-__device__ __forceinline__ void tc_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(acc));
-}
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-
-// Shared-memory matrix descriptors, K-major: 128B swizzle (8-row groups 1024 B apart) and
-// 32B swizzle (8-row groups 256 B apart).
-__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
-    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)(1024u >> 4) << 32) | (1ull << 46) | (2ull << 61);
-}
-__device__ __forceinline__ uint64_t desc_sw32(uint32_t saddr) {
-    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)(256u >> 4) << 32) | (1ull << 46) | (6ull << 61);
-}
-
-// Instruction descriptor: D fp32, A/B f16 (KIND 0) or tf32 (KIND 1), both K-major, M=128, N=BN.
-template <int KIND>
-__host__ __device__ constexpr uint32_t instr_desc() {
-    return (1u << 4) | ((KIND ? 2u : 0u) << 7) | ((KIND ? 2u : 0u) << 10) | ((BN >> 3) << 17) | ((MSUB >> 4) << 24);
-}
-
-// (a - t, b - t) with one packed FADD2 (sm_100); results as raw bits
-__device__ __forceinline__ void sub2(uint32_t a, uint32_t b, float t, uint32_t& ra, uint32_t& rb) {
-    asm("{\n\t.reg .b64 x, y, z;\n\t"
-        "mov.b64 x, {%2, %3};\n\t"
-        "mov.b64 y, {%4, %4};\n\t"
-        "sub.rn.f32x2 z, x, y;\n\t"
-        "mov.b64 {%0, %1}, z;\n\t}"
-        : "=r"(ra), "=r"(rb)
-        : "r"(a), "r"(b), "r"(__float_as_uint(t)));
-}
-
-__device__ __forceinline__ float next_up(float x) {   // smallest float > x (x < +inf)
-    return x == __int_as_float(0x7f800000) ? x : ord2f(f2ord(x) + 1u);
-}
-
-struct KnnParams {
-    const float* norm_a;       // |a_i|^2 (0 for IP) for the final distance, operand row order
-    uint64_t* cand;            // gridDim.x * BM rows * C candidate words
-    uint32_t* out_ids;         // ma x L
-    float* out_d;              // ma x L
-    float* probe;              // optional raw accumulator dump (ma x mb)
-    unsigned long long* prof;  // optional per-warp cycle counters (diagnostics)
-    const uint32_t* row_map;   // A row (operand order) -> output row (nullptr = identity)
-    const uint32_t* col_map;   // B row (operand order) -> reported id (nullptr = identity)
-    uint32_t ma, mb, L, C, n_rb, n_ct, stages;
-    uint32_t rb_rows;          // rows per row block (128 * accumulators)
-    uint32_t t_back;           // with rotate: a row block starts t_back tiles before its diagonal
-    int rotate;                // column tiles visited from the diagonal - t_back cyclically
-    int self_exclude;
-    int noepi;                 // diagnostics: epilogue only drains TMEM (pipeline speed test)
-    int noload;                // diagnostics: producer skips the B loads (tensor-core speed test)
-    int abl;                   // diagnostics ablation bits: 1 no insertion, 2 no id fetch, 4 no clock64
-    const uint4* a_glob;       // A side operand rows (for A-in-TMEM), kdim halves per row
-    uint32_t a_words;          // 32-bit words per A row
-};
-
-__device__ __forceinline__ uint32_t tile_at(const KnnParams& p, uint32_t rb, uint32_t i) {
-    if (!p.rotate) return i;
-    const uint32_t diag = rb * (p.rb_rows / BN) % p.n_ct;
-    const uint32_t back = p.t_back % p.n_ct;
-    return (diag + p.n_ct - back + i) % p.n_ct;
-}
-
-struct __align__(8) Bars {
-    uint64_t full[MAX_STAGES], empty[MAX_STAGES];
-    uint64_t a_full, a_empty;
-    uint64_t tm_full[NBUF_MAX], tm_empty[NBUF_MAX];
-    uint32_t tmem_base;
-};
-
-// Candidate words are stored raw as (float bits << 32 | col); selection works on the ordered
-// form (ord(key) << 32 | col) whose unsigned order is the (key, col) order.
-__device__ __forceinline__ uint64_t raw2ord(uint64_t w) {
-    return ((uint64_t)f2ord(__uint_as_float((uint32_t)(w >> 32))) << 32) | (uint32_t)w;
-}
-__device__ __forceinline__ uint64_t ord2raw(uint64_t w) {
-    return ((uint64_t)__float_as_uint(ord2f((uint32_t)(w >> 32))) << 32) | (uint32_t)w;
-}
-
-__device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const uint64_t t = __shfl_xor_sync(0xffffffffu, v, o);
-        v = t < v ? t : v;
-    }
-    return v;
-}
-__device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const uint64_t t = __shfl_xor_sync(0xffffffffu, v, o);
-        v = t > v ? t : v;
-    }
-    return v;
-}
-
-// Warp-cooperative radix selection over rb[0..cnt) (cnt > L).  Keeps, in place at rb[0..kept), a
-// prefix of the (key, id) order with L <= kept <= keep_max (keep_max = L: exactly the L smallest)
-// and returns the largest kept key (ordered u32).  8-bit digits start at the highest bit where the
-// smallest and largest candidate differ (the shared prefix would put every candidate in one
-// histogram bin), counted with shared-memory atomics.  All 32 lanes call with the same arguments.
-template <int EPL>
-__device__ __forceinline__ uint32_t select_L(uint64_t* rb, uint32_t cnt, uint32_t L, uint32_t keep_max,
-                                             uint32_t* hist, uint32_t lane, uint32_t* kept) {
-    uint64_t e[EPL];
-    uint64_t lo = ~0ull, hi = 0;
-#pragma unroll
-    for (int i = 0; i < EPL; i++) {
-        const uint32_t idx = i * 32 + lane;
-        e[i] = idx < cnt ? raw2ord(rb[idx]) : ~0ull;
-        if (idx < cnt) { lo = e[i] < lo ? e[i] : lo; hi = e[i] > hi ? e[i] : hi; }
-    }
-    lo = warp_min_u64(lo);
-    hi = warp_max_u64(hi);
-    // bits [top, 64) are common to every candidate
-    int top = 64 - __clzll(lo ^ hi);              // 0 only if all equal (cannot happen: ids differ)
-    uint64_t pfx = top >= 64 ? 0ull : (lo >> top) << top;
-    uint32_t want = L;
-    int cut = top;
-    uint32_t kp = 0;
-#pragma unroll 1
-    while (top > 0) {
-        const int w = top >= 8 ? 8 : top;          // digit = bits [top - w, top)
-        const int sh = top - w;
-        for (int b = lane; b < 256; b += 32) hist[b] = 0;
-        __syncwarp();
-        const uint64_t hm = top >= 64 ? 0ull : (~0ull << top);
-        const uint32_t dmask = (1u << w) - 1u;
-#pragma unroll
-        for (int i = 0; i < EPL; i++)
-            if (e[i] != ~0ull && (e[i] & hm) == (pfx & hm)) atomicAdd(&hist[(uint32_t)(e[i] >> sh) & dmask], 1u);
-        __syncwarp();
-        uint32_t hv[8], loc = 0;
-#pragma unroll
-        for (int j = 0; j < 8; j++) { hv[j] = hist[lane * 8 + j]; loc += hv[j]; }
-        const uint32_t inc = warp_incl_scan(loc, lane), exc = inc - loc;
-        const bool mine = exc < want && want <= inc;
-        const uint32_t bal = __ballot_sync(0xffffffffu, mine);
-        uint32_t dg = 0, before = 0, bc = 0;
-        if (mine) {
-            uint32_t run = exc;
-#pragma unroll
-            for (int j = 0; j < 8; j++) {
-                if (bc == 0 && run + hv[j] >= want) { dg = lane * 8 + j; before = run; bc = hv[j]; }
-                run += hv[j];
-            }
-        }
-        const int src = __ffs(bal) - 1;
-        dg = __shfl_sync(0xffffffffu, dg, src);
-        before = __shfl_sync(0xffffffffu, before, src);
-        bc = __shfl_sync(0xffffffffu, bc, src);
-        want -= before;
-        pfx |= (uint64_t)dg << sh;
-        __syncwarp();
-        top = sh;
-        // entries strictly below the chosen bucket: L - want; cutting here keeps the bucket too
-        if (L - want + bc <= keep_max || top == 0) { cut = sh; kp = L - want + bc; break; }
-    }
-    const uint64_t lim = cut >= 64 ? ~0ull : pfx >> cut;
-    uint32_t base = 0, mk = 0;
-    __syncwarp();
-#pragma unroll
-    for (int i = 0; i < EPL; i++) {
-        const uint32_t idx = i * 32 + lane;
-        const bool s = idx < cnt && (cut >= 64 || (e[i] >> cut) <= lim);
-        const uint32_t bal = __ballot_sync(0xffffffffu, s);
-        if (s) {
-            rb[base + __popc(bal & ((1u << lane) - 1u))] = ord2raw(e[i]);
-            mk = max(mk, (uint32_t)(e[i] >> 32));
-        }
-        base += __popc(bal);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mk = max(mk, __shfl_xor_sync(0xffffffffu, mk, o));
-    __syncwarp();
-    *kept = base;
-    (void)kp;
-    return mk;
-}
-
-// Merge the two column halves' survivors of one row (each <= L), sort by (dist, id) with
-// dist = |a_i|^2 + key, write the first L (sentinel / +inf padding).
-__device__ void finish_row(const uint64_t* b0, uint32_t c0, const uint64_t* b1, uint32_t c1, uint32_t L,
-                           uint64_t* sortbuf, float na, uint32_t* out_ids, float* out_d, uint32_t lane) {
-    const uint32_t cnt = c0 + c1;
-    uint32_t np = 32;
-    while (np < cnt) np <<= 1;
-    for (uint32_t p = lane; p < np; p += 32) {
-        uint64_t w = ~0ull;
-        if (p < cnt) {
-            const uint64_t e = p < c0 ? b0[p] : b1[p - c0];
-            const float dist = na + __uint_as_float((uint32_t)(e >> 32));
-            w = ((uint64_t)f2ord(dist) << 32) | (uint32_t)e;
-        }
-        sortbuf[p] = w;
-    }
-    __syncwarp();
-    warp_sort_u64(sortbuf, np, lane);
-    for (uint32_t p = lane; p < L; p += 32) {
-        const uint64_t w = sortbuf[p];
-        out_ids[p] = p < cnt ? (uint32_t)w : SG_SENT;
-        out_d[p] = p < cnt ? ord2f((uint32_t)(w >> 32)) : __int_as_float(0x7f800000);
-    }
-    __syncwarp();
-}
 
 // ----------------------------------------------------------------- the kernel
 template <int KIND, int NKA, int MINI, int EPL>
@@ -352,14 +44,21 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     constexpr bool ATM = KIND == 0 && SG_ATM;
     constexpr uint32_t NBUF = ATM ? 2 : 512 / (NACC * BN);
     constexpr uint32_t AHALF = ATM ? 0u : NKA * ATOM + (MINI ? MINIB : 0u);   // smem bytes of one 128-row half
-    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    // offsets from smem_raw (not integer casts) so the compiler keeps shared-space accesses (LDS/STS)
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sA = smem;                                    // [NACC][NKA atoms + mini] (SS mode)
     uint8_t* sB = smem + NACC * AHALF;
     Bars* bars = (Bars*)(sB + p.stages * SLOT);
-    uint8_t* scratch_all = (uint8_t*)(((uintptr_t)(bars + 1) + 127) & ~(uintptr_t)127);   // NEPI x SCRATCH
+    uint8_t* bars_end = (uint8_t*)(bars + 1);
+    uint8_t* scratch_all = bars_end + ((128u - (smem_u32(bars_end) & 127u)) & 127u);   // NEPI x SCRATCH
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    long long pw[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // cycle counters + event counts (diagnostics)
+    // fallback launch: the number of A rows is known only on the device
+    const uint32_t ma = p.n_rows_dev ? *(const volatile uint32_t*)p.n_rows_dev : p.ma;
+    const uint32_t n_rb = (ma + RB - 1) / RB;
+    constexpr bool PROF = SG_KNN_PROF != 0;
+    long long pw[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // cycle counters + event counts (PROF builds only)
+    auto clk = []() -> long long { return PROF ? clock64() : 0ll; };
 
     if (threadIdx.x == 0) {
         for (uint32_t s = 0; s < p.stages; s++) { mbar_init(&bars->full[s], 1); mbar_init(&bars->empty[s], 1); }
@@ -391,7 +90,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         // ===================== TMA producer =====================
         if (lane == 0) {
             uint32_t stage = 0, sph = 0, it = 0;
-            for (uint32_t rb = blockIdx.x; rb < p.n_rb; rb += gridDim.x, it++) {
+            for (uint32_t rb = blockIdx.x; rb < n_rb; rb += gridDim.x, it++) {
                 if (!ATM) {
                     if (it > 0) mbar_wait(&bars->a_empty, (it - 1) & 1);
                     mbar_expect_tx(&bars->a_full, NACC * AHALF);
@@ -402,9 +101,8 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                         tma_load_2d(&tmA, &bars->a_full, base + ka * ATOM, ka * ATOM_K, rb * RB + a * MSUB);
                     if (MINI) tma_load_2d(&tmAm, &bars->a_full, base + NKA * ATOM, NKA * ATOM_K, rb * RB + a * MSUB);
                 }
-                for (uint32_t ti = 0; ti < p.n_ct; ti++) {
-                    const uint32_t t = tile_at(p, rb, ti);
-                    long long w0 = clock64();
+                for (uint32_t ti = 0, t = tile_at(p, rb, 0); ti < p.n_ct; ti++, t = t + 1 == p.n_ct ? 0 : t + 1) {
+                    long long w0 = clk();
 #pragma unroll
                     for (uint32_t ka = 0; ka < NSLOT; ka++) {
                         mbar_wait(&bars->empty[stage], sph ^ 1);
@@ -419,7 +117,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                         }
                         if (++stage == p.stages) { stage = 0; sph ^= 1; }
                     }
-                    pw[0] += clock64() - w0;
+                    pw[0] += clk() - w0;
                 }
             }
         }
@@ -429,20 +127,20 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             constexpr uint32_t idesc = instr_desc<KIND>();
             const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
             uint32_t stage = 0, sph = 0, it = 0, git = 0;
-            for (uint32_t rb = blockIdx.x; rb < p.n_rb; rb += gridDim.x, it++) {
+            for (uint32_t rb = blockIdx.x; rb < n_rb; rb += gridDim.x, it++) {
                 mbar_wait(&bars->a_full, it & 1);
                 tc_fence_after();
                 for (uint32_t ti = 0; ti < p.n_ct; ti++, git++) {
                     const uint32_t buf = git % NBUF;
-                    const long long w0 = clock64();
+                    const long long w0 = clk();
                     mbar_wait(&bars->tm_empty[buf], ((git / NBUF) & 1) ^ 1);
-                    pw[0] += clock64() - w0;
+                    pw[0] += clk() - w0;
                     tc_fence_after();
 #pragma unroll
                     for (uint32_t ka = 0; ka < NSLOT; ka++) {
-                        const long long w1 = clock64();
+                        const long long w1 = clk();
                         mbar_wait(&bars->full[stage], sph);
-                        pw[1] += clock64() - w1;
+                        pw[1] += clk() - w1;
                         tc_fence_after();
                         const uint32_t bslot = b_base + stage * SLOT;
 #pragma unroll
@@ -488,15 +186,16 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         uint64_t* sortbuf = (uint64_t*)scratch;              // 512 (aliases skeys)
         uint32_t* sids = (uint32_t*)(scratch + 32 * KSTRIDE * 4);   // 64 reported ids of the tile
         const uint32_t C = p.C;
-        const uint32_t keep_max = p.L + (C - 32 - p.L) / 8;  // approximate in-loop compaction target
+        const uint32_t keep_max = p.keep_max;                // in-loop compaction target (>= L)
         uint64_t* myrow = p.cand + ((uint64_t)blockIdx.x * BM + r) * C;
         uint64_t* warprows = p.cand + ((uint64_t)blockIdx.x * BM + a * MSUB + q * 32) * C;
         const float INF = __int_as_float(0x7f800000);
         const uint32_t tl = tmem + ((q * 32) << 16) + a * NBUF * BN;
         uint32_t git = 0;
-        for (uint32_t rb = blockIdx.x; rb < p.n_rb && a < NACC; rb += gridDim.x) {
+        for (uint32_t rb = blockIdx.x; rb < n_rb && a < NACC; rb += gridDim.x) {
             const uint32_t row = rb * RB + r;
-            const bool valid = row < p.ma;
+            const bool valid = row < ma;
+            const uint32_t scol = p.self_exclude ? (p.self_col ? (valid ? p.self_col[row] : SG_SENT) : row) : SG_SENT;
             float thr = valid ? INF : -INF;
             uint32_t cnt = 0;
             if constexpr (ATM) {
@@ -514,12 +213,11 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->a_full);
             }
-            for (uint32_t ti = 0; ti < p.n_ct; ti++, git++) {
-                const uint32_t t = tile_at(p, rb, ti);
+            for (uint32_t ti = 0, t = tile_at(p, rb, 0); ti < p.n_ct; ti++, git++, t = t + 1 == p.n_ct ? 0 : t + 1) {
                 const uint32_t buf = git % NBUF;
-                long long c0 = clock64();
+                long long c0 = clk();
                 mbar_wait(&bars->tm_full[buf], (git / NBUF) & 1);
-                long long c1 = clock64();
+                long long c1 = clk();
                 pw[0] += c1 - c0;
                 tc_fence_after();
                 const uint32_t tb = tl + buf * BN;
@@ -540,12 +238,12 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&bars->tm_empty[buf]);
                     }
-                    c0 = clock64();
+                    c0 = clk();
                     pw[1] += c0 - c1;
                     const uint32_t col0 = t * BN + hp * 32;
                     if (p.noepi) {
                         if ((v[0] ^ v[31]) == 0x7fc00001u) p.out_ids[0] = v[1];   // keep the loads live
-                        c1 = clock64();
+                        c1 = clk();
                         continue;
                     }
                     if (p.probe) {
@@ -554,24 +252,12 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                             for (int j = 0; j < 32; j++)
                                 if (col0 + j < p.mb) p.probe[(uint64_t)row * p.mb + col0 + j] = __uint_as_float(v[j]);
                         }
-                        c1 = clock64();
+                        c1 = clk();
                         continue;
                     }
                     // reported id of this lane's column, fetched early (latency hidden by the mask)
-                    const uint32_t id0 = (p.col_map && !(p.abl & 2)) ? __ldg(p.col_map + col0 + lane) : col0 + lane;
-                    // make room: rows whose buffer cannot take another 32 candidates are compacted
-                    uint32_t need = __ballot_sync(0xffffffffu, cnt > C - 32);
-                    while (need) {
-                        const int o = __ffs(need) - 1;
-                        need &= need - 1;
-                        const uint32_t c_o = __shfl_sync(0xffffffffu, cnt, o);
-                        uint32_t kept;
-                        const uint32_t kth =
-                            select_L<EPL>(warprows + (uint64_t)o * C, c_o, p.L, keep_max, hist, lane, &kept);
-                        if (lane == (uint32_t)o) { cnt = kept; thr = ord2f(kth); }
-                    }
-                    c1 = clock64();
-                    pw[2] += c1 - c0;   // compaction
+                    const uint32_t id0 = p.col_map ? __ldg(p.col_map + col0 + lane) : col0 + lane;
+                    c1 = clk();
                     // strict test when columns arrive in increasing id, inclusive with the rotated sweep
                     const float te = p.rotate ? next_up(thr) : thr;
                     uint32_t mq[4] = {0, 0, 0, 0};
@@ -588,8 +274,8 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     }
                     uint32_t m = mq[0] | (mq[1] << 8) | (mq[2] << 16) | (mq[3] << 24);
                     // self column: row r of block rb is column rb*RB + r
-                    if (p.self_exclude && col0 <= row && row < col0 + 32) m &= ~(1u << (row - col0));
-                    c0 = clock64();
+                    if (scol - col0 < 32u) m &= ~(1u << (scol - col0));
+                    c0 = clk();
                     pw[3] += c0 - c1;   // masks
                     if (p.abl & 1) m = 0;
                     if (__any_sync(0xffffffffu, m != 0)) {
@@ -600,42 +286,86 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                             st4[j4] = make_float4(__uint_as_float(v[4 * j4]), __uint_as_float(v[4 * j4 + 1]),
                                                   __uint_as_float(v[4 * j4 + 2]), __uint_as_float(v[4 * j4 + 3]));
                         __syncwarp();
-                        pw[6] += __popc(m);
+                        if constexpr (PROF) pw[6] += __popc(m);
+                        // two candidates per iteration: independent smem loads and global stores
+                        const float* mykeys = skeys + lane * KSTRIDE;
                         while (m) {
-                            pw[7]++;
-                            const uint32_t c = 31 - __clz(m);
-                            m ^= 1u << c;
-                            const uint32_t kb = __float_as_uint(skeys[lane * KSTRIDE + c]);
-                            myrow[cnt++] = ((uint64_t)kb << 32) | sids[c];
+                            if constexpr (PROF) pw[7]++;
+                            const uint32_t b0 = 31 - __clz(m);
+                            m ^= 1u << b0;
+                            const bool two = m != 0;
+                            const uint32_t b1 = two ? 31 - __clz(m) : b0;
+                            m &= ~(1u << b1);
+                            const uint32_t k0 = __float_as_uint(mykeys[b0]), i0 = sids[b0];
+                            const uint32_t k1 = __float_as_uint(mykeys[b1]), i1 = sids[b1];
+                            myrow[cnt] = ((uint64_t)k0 << 32) | i0;
+                            if (two) myrow[cnt + 1] = ((uint64_t)k1 << 32) | i1;
+                            cnt += two ? 2 : 1;
                         }
                         __syncwarp();
                     }
-                    c1 = clock64();
+                    c1 = clk();
                     pw[4] += c1 - c0;   // insertions
+                    // make room: rows whose buffer cannot take another pass are compacted to the
+                    // target rank (L, or the extrapolated rank for the fraction of columns seen)
+                    uint32_t need = __ballot_sync(0xffffffffu, cnt > C - 32);
+                    if (need) {
+                        uint32_t want = p.L, kmax = keep_max;
+                        if (p.alpha100) {
+                            const uint64_t seen = (uint64_t)ti * BN + (hp + 1) * 32;
+                            const uint64_t rr = (uint64_t)p.alpha100 * p.L * seen / (100ull * p.mb) + p.beta;
+                            if (rr < p.L) { want = (uint32_t)rr; kmax = want + (C - 32 - want) / 8; }
+                        }
+                        do {
+                            const int o = __ffs(need) - 1;
+                            need &= need - 1;
+                            const uint32_t c_o = __shfl_sync(0xffffffffu, cnt, o);
+                            uint64_t* ob = warprows + (uint64_t)o * C;
+                            uint32_t kept;
+                            uint32_t kth = select_keys<EPL>(ob, c_o, want, kmax, lane, &kept);
+                            // massive ties on the threshold key: split them by id (prefix of (key, id))
+                            if (kept > C - 32)
+                                kth = (uint32_t)(select_L<EPL>(ob, kept, want, kmax, hist, lane, &kept) >> 32);
+                            if (lane == (uint32_t)o) { cnt = kept; thr = ord2f(kth); }
+                        } while (need);
+                    }
+                    c0 = clk();
+                    pw[2] += c0 - c1;   // compaction
                 }
             }
             if (p.probe || p.noepi) continue;
-            const long long f0 = clock64();
+            const long long f0 = clk();
             // ---- final: exact top-L of each of the warp's rows, sorted by (dist, id)
             __syncwarp();
             for (uint32_t o = 0; o < 32; o++) {
                 uint32_t c_o = __shfl_sync(0xffffffffu, cnt, o);
                 const uint32_t row_o = rb * RB + a * MSUB + q * 32 + o;
-                if (row_o >= p.ma) continue;
+                if (row_o >= ma) continue;
+                if (p.alpha100 && c_o < p.L) {
+                    // extrapolated threshold was too tight for this row: recompute it (fallback)
+                    if (lane == 0) p.fail_rows[atomicAdd(p.fail_count, 1u)] = row_o;
+                    continue;
+                }
                 uint64_t* b0 = warprows + (uint64_t)o * C;
                 if (c_o > p.L) {
+                    // every key <= the L-th smallest key (finish_row sorts them and writes L);
+                    // exact (key, id) selection only if ties would overflow the sort buffer
                     uint32_t kept;
-                    select_L<EPL>(b0, c_o, p.L, p.L, hist, lane, &kept);
-                    c_o = p.L;
+                    select_keys<EPL>(b0, c_o, p.L, p.L, lane, &kept);
+                    if (kept > SORT_MAX) {
+                        select_L<EPL>(b0, kept, p.L, p.L, hist, lane, &kept);
+                        kept = p.L;
+                    }
+                    c_o = kept;
                 }
                 const uint64_t orow = p.row_map ? p.row_map[row_o] : row_o;
                 finish_row(b0, c_o, b0, 0, p.L, sortbuf, p.norm_a[row_o], p.out_ids + orow * p.L,
                            p.out_d + orow * p.L, lane);
             }
-            pw[5] += clock64() - f0;   // final phase
+            pw[5] += clk() - f0;   // final phase
         }
     }
-    if (p.prof && lane == 0)
+    if (PROF && p.prof && lane == 0)
         for (int i = 0; i < 8; i++) atomicAdd(p.prof + warp * 8 + i, (unsigned long long)pw[i]);
     tc_fence_before();
     __syncthreads();
@@ -645,40 +375,21 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     }
 }
 
-// ----------------------------------------------------------------- host side
-PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    if (!fn) {
-        cudaDriverEntryPointQueryResult qr;
-        void* ptr = nullptr;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &qr) == cudaSuccess &&
-            qr == cudaDriverEntryPointSuccess)
-            fn = (PFN_cuTensorMapEncodeTiled_v12000)ptr;
-    }
-    return fn;
-}
-
-// 2-D map over a rows x kdim operand; box = (box_bytes / esize) elements x box_rows rows.
-sg_status make_map(CUtensorMap* m, const void* base, uint64_t rows, uint32_t kdim, uint32_t esize, uint32_t box_bytes,
-                   uint32_t box_rows) {
-    auto enc = get_encode();
-    if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return SG_ERR_CUDA; }
-    cuuint64_t dims[2] = {kdim, rows};
-    cuuint64_t strides[1] = {(cuuint64_t)kdim * esize};
-    cuuint32_t box[2] = {box_bytes / esize, box_rows};
-    cuuint32_t es[2] = {1, 1};
-    const CUtensorMapSwizzle sw = box_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B;
-    CUresult r = enc(m, esize == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
-                     const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) { set_error("cuTensorMapEncodeTiled failed (%d)", (int)r); return SG_ERR_CUDA; }
-    return SG_OK;
-}
-
+// Candidate buffer words per row: room for one 32-column pass above the kept set (>= L + 32).
+// SG_KNN_C overrides (tuning); SG_KNN_KEEP=1 makes in-loop compaction exact (keep L).
 uint32_t cand_cap(uint32_t L) {
-    uint32_t c = 256;   // > BN + L: room for one tile of candidates above the kept set
-    while (c < 4 * L && c < 1024) c <<= 1;
+    static int env = -1;
+    if (env < 0) { const char* e = getenv("SG_KNN_C"); env = e ? atoi(e) : 0; }
+    uint32_t c = 256;
+    while (c < 2 * L && c < 1024) c <<= 1;
+    if (env > 0) c = (uint32_t)env < 1024u ? (uint32_t)env : 1024u;
+    while (c < L + 64) c <<= 1;
     return c;
+}
+uint32_t keep_target(uint32_t L, uint32_t C) {
+    static int env = -1;
+    if (env < 0) { const char* e = getenv("SG_KNN_KEEP"); env = e ? atoi(e) : 0; }
+    return env == 1 ? L : L + (C - 32 - L) / 8;
 }
 
 template <int KIND, int NKA, int MINI, int EPL>
@@ -726,9 +437,71 @@ void set_knn_profile(unsigned long long* buf) { g_knn_prof = buf; }
 
 uint32_t knn_row_align() { return BM; }
 
-size_t knn_core_workspace(uint32_t L) {
-    return (size_t)num_sms() * BM * cand_cap(L) * sizeof(uint64_t) + 4096;
+// transposed kernel (knn_tct.cu): L <= 128, selected unless SG_KNN_T=0
+uint32_t knn_t_cap(uint32_t L, bool extrap);
+sg_status launch_knn_t(const CUtensorMap* maps, KnnParams& p, int esize, int nka, int mini, cudaStream_t st);
+static bool use_transposed(uint32_t L) {
+    static int on = -1;
+    if (on < 0) { const char* e = getenv("SG_KNN_T"); on = e ? atoi(e) : 0; }
+    return on && L <= 128;
 }
+static size_t cand_words_per_cta(uint32_t L) {
+    const size_t row_major = (size_t)BM * cand_cap(L);
+    const size_t transposed = use_transposed(L) ? (size_t)BM * 4 * knn_t_cap(L, false) : 0;
+    return row_major > transposed ? row_major : transposed;
+}
+
+size_t knn_core_workspace(uint32_t L, uint64_t ma, uint32_t d, int prec, int metric) {
+    // candidate buffers + fallback state (failed-row list, copy of their A rows)
+    return (size_t)num_sms() * cand_words_per_cta(L) * sizeof(uint64_t) + 2 * ((ma + BM) * 4 + 256) +
+           operand_bytes(prec, metric, d, ma, SIDE_A) + 8192;
+}
+
+namespace {
+// A2 row i = A row fail_rows[i] (the rows the extrapolated launch could not finish); the count is
+// read on the device, so the fallback needs no host synchronisation.
+__global__ void copy_fail_rows(const uint32_t* __restrict__ a, const float* __restrict__ norm, uint32_t words,
+                               const uint32_t* __restrict__ fail_rows, const uint32_t* __restrict__ fail_count,
+                               uint32_t* __restrict__ a2, float* __restrict__ norm2) {
+    const uint32_t cnt = *fail_count;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t i = warp; i < cnt; i += nw) {
+        const uint32_t r = fail_rows[i];
+        for (uint32_t w = lane; w < words; w += 32) a2[(uint64_t)i * words + w] = a[(uint64_t)r * words + w];
+        if (lane == 0) norm2[i] = norm[r];
+    }
+}
+
+int env_int(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+
+sg_status launch_knn(const Operand& A, const Operand& B, KnnParams& p, cudaStream_t st) {
+    CUtensorMap maps[4];
+    SG_TRY(make_map(&maps[0], A.a, A.rows_pad, A.kdim, A.esize, 128, MSUB));
+    SG_TRY(make_map(&maps[1], B.b, B.rows_pad, B.kdim, B.esize, 128, BN));
+    if (A.mini) {
+        SG_TRY(make_map(&maps[2], A.a, A.rows_pad, A.kdim, A.esize, 32, MSUB));
+        SG_TRY(make_map(&maps[3], B.b, B.rows_pad, B.kdim, B.esize, 32, BN));
+    } else {
+        maps[2] = maps[0];
+        maps[3] = maps[1];
+    }
+    const int epl = (int)(p.C / 32);
+    const int nka = (int)A.nfull, mini = (int)A.mini;
+    if (use_transposed(p.L)) return launch_knn_t(maps, p, (int)A.esize, nka, mini, st);
+    if (A.esize == 4) {
+        if (epl <= 8) return launch_mini<1, 8>(nka, mini, maps, p, st);
+        if (epl <= 16) return launch_mini<1, 16>(nka, mini, maps, p, st);
+        return launch_mini<1, 32>(nka, mini, maps, p, st);
+    }
+    if (epl <= 8) return launch_mini<0, 8>(nka, mini, maps, p, st);
+    if (epl <= 16) return launch_mini<0, 16>(nka, mini, maps, p, st);
+    return launch_mini<0, 32>(nka, mini, maps, p, st);
+}
+}  // namespace
 
 sg_status knn_core(const Operand& A, const Operand& B, int /*metric*/, bool self_exclude, uint32_t L, uint32_t* ids,
                    float* dists, float* probe, Carver& cv, cudaStream_t st, const uint32_t* row_map,
@@ -743,7 +516,8 @@ sg_status knn_core(const Operand& A, const Operand& B, int /*metric*/, bool self
     p.a_glob = (const uint4*)A.a;
     p.a_words = A.kdim * A.esize / 4;
     p.C = cand_cap(L);
-    p.cand = cv.take<uint64_t>((size_t)num_sms() * BM * p.C);
+    p.keep_max = keep_target(L, p.C);
+    p.cand = cv.take<uint64_t>((size_t)num_sms() * cand_words_per_cta(L));
     if (!cv.ok()) { set_error("kNN: workspace too small"); return SG_ERR_WORKSPACE; }
     p.out_ids = ids;
     p.out_d = dists;
@@ -759,40 +533,53 @@ sg_status knn_core(const Operand& A, const Operand& B, int /*metric*/, bool self
     p.row_map = row_map;
     p.col_map = col_map;
     p.rotate = rotate ? 1 : 0;
-    {
-        static int tb = -1;
-        if (tb < 0) { const char* e = getenv("SG_TBACK"); tb = e ? atoi(e) : 8; }
-        p.t_back = (uint32_t)tb;
-        static int ne = -1;
-        if (ne < 0) { const char* e = getenv("SG_KNN_NOEPI"); ne = e ? atoi(e) : 0; }
-        p.noepi = ne && rotate;   // only the main (reordered) sweep; the order pass needs its result
-        static int nl = -1;
-        if (nl < 0) { const char* e = getenv("SG_KNN_NOLOAD"); nl = e ? atoi(e) : 0; }
-        p.noload = nl && rotate && ne;
-        static int ab = -1;
-        if (ab < 0) { const char* e = getenv("SG_KNN_ABL"); ab = e ? atoi(e) : 0; }
-        p.abl = rotate ? ab : 0;
+    static const int tb = env_int("SG_TBACK", 8), ne = env_int("SG_KNN_NOEPI", 0), nl = env_int("SG_KNN_NOLOAD", 0),
+                     ab = env_int("SG_KNN_ABL", 0), alpha = env_int("SG_KNN_ALPHA", 150),
+                     beta = env_int("SG_KNN_BETA", -1), report = env_int("SG_KNN_REPORT", 0),
+                     eager = env_int("SG_KNN_EAGER", 16);
+    p.t_back = (uint32_t)tb;
+    const bool main_sweep = L > 1 && !probe;          // not the spatial-order assignment pass
+    p.noepi = ne && main_sweep;
+    p.noload = nl && p.noepi;
+    p.abl = main_sweep ? ab : 0;
+    // extrapolated thresholds need columns in an order unrelated to the rows' positions
+    const bool extrap = main_sweep && !rotate && !row_map && alpha > 0 && B.rows >= 4ull * L && !p.noepi;
+    const bool tr = use_transposed(L);
+    if (tr) p.C = knn_t_cap(L, extrap);
+    if (!extrap) return launch_knn(A, B, p, st);
+
+    uint32_t* fail_count = cv.take<uint32_t>(1);
+    uint32_t* fail_rows = cv.take<uint32_t>(A.rows_pad);
+    Operand A2 = A;
+    A2.a = cv.take<uint8_t>((size_t)A.rows_pad * A.kdim * A.esize);
+    A2.norm = cv.take<float>(A.rows_pad);
+    if (!cv.ok()) { set_error("kNN: workspace too small (fallback)"); return SG_ERR_WORKSPACE; }
+    SG_CUDA(cudaMemsetAsync(fail_count, 0, sizeof(uint32_t), st));
+    p.alpha100 = (uint32_t)alpha;
+    p.beta = (uint32_t)(beta >= 0 ? beta : tr ? 6 : 8);   // per stream (transposed) / per row
+    p.eager = (uint32_t)eager;
+    p.fail_count = fail_count;
+    p.fail_rows = fail_rows;
+    SG_TRY(launch_knn(A, B, p, st));
+    if (report) {
+        uint32_t h = 0;
+        cudaMemcpyAsync(&h, fail_count, sizeof(h), cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        fprintf(stderr, "[knn] extrapolated thresholds: %u of %llu rows recomputed\n", h, (unsigned long long)A.rows);
     }
-    CUtensorMap maps[4];
-    SG_TRY(make_map(&maps[0], A.a, A.rows_pad, A.kdim, A.esize, 128, MSUB));
-    SG_TRY(make_map(&maps[1], B.b, B.rows_pad, B.kdim, B.esize, 128, BN));
-    if (A.mini) {
-        SG_TRY(make_map(&maps[2], A.a, A.rows_pad, A.kdim, A.esize, 32, MSUB));
-        SG_TRY(make_map(&maps[3], B.b, B.rows_pad, B.kdim, B.esize, 32, BN));
-    } else {
-        maps[2] = maps[0];
-        maps[3] = maps[1];
-    }
-    const int epl = (int)(p.C / 32);
-    const int nka = (int)A.nfull, mini = (int)A.mini;
-    if (A.esize == 4) {
-        if (epl <= 8) return launch_mini<1, 8>(nka, mini, maps, p, st);
-        if (epl <= 16) return launch_mini<1, 16>(nka, mini, maps, p, st);
-        return launch_mini<1, 32>(nka, mini, maps, p, st);
-    }
-    if (epl <= 8) return launch_mini<0, 8>(nka, mini, maps, p, st);
-    if (epl <= 16) return launch_mini<0, 16>(nka, mini, maps, p, st);
-    return launch_mini<0, 32>(nka, mini, maps, p, st);
+    // fallback: the failed rows, plain rank-L thresholds, results to their own output rows
+    copy_fail_rows<<<num_sms() * 4, 256, 0, st>>>((const uint32_t*)A.a, A.norm, p.a_words, fail_rows, fail_count,
+                                                  (uint32_t*)A2.a, A2.norm);
+    SG_LAUNCHED("copy_fail_rows");
+    KnnParams p2 = p;
+    p2.alpha100 = 0;
+    if (tr) p2.C = knn_t_cap(L, false);
+    p2.norm_a = A2.norm;
+    p2.a_glob = (const uint4*)A2.a;
+    p2.n_rows_dev = fail_count;
+    p2.row_map = fail_rows;
+    p2.self_col = self_exclude ? fail_rows : nullptr;
+    return launch_knn(A2, B, p2, st);
 }
 
 }  // namespace sg

@@ -1,0 +1,494 @@
+// a5 — exact kNN, transposed tiles (L <= 128): tcgen05 distance tiles with the streamed columns
+// on the MMA's M side, so that the per-row top-L runs on warp ballots (north_star stage 2).
+//
+// The distance key is the same augmented contraction as knn_tc.cu (key(i, j) = |b_j|^2 - 2 a_i.b_j,
+// exact in fp32 for integer data; reading R3), but the roles are swapped: one M=128 x N=RB MMA
+// per K step takes 128 streamed columns j as M (TMEM lanes) and the CTA's RB resident rows i as N
+// (TMEM columns).  A 32x32b TMEM load then gives each thread one COLUMN and each register one
+// ROW, so one FSETP + one VOTE.ballot yields the 32-bit candidate mask of a row over 32 columns
+// (1/16 instruction per key instead of 1.5), and the candidates of a row are appended with one
+// coalesced store per row.
+//
+// Each epilogue warp sees one TMEM lane quadrant = 32 of the 128 columns of a tile, so a row has
+// NS = 4 candidate streams (column j goes to stream (j / 32) % 4), each with its own buffer, and
+// ONE threshold pair (key, id) per row shared by its streams: when a stream compacts its buffer
+// to a prefix of the (key, id) order it lowers the row's pair with a shared-memory atomicMin;
+// the ballot test reads a float copy of the key (key <= thr; equal keys are filtered by the
+// pair), which may be stale but is never below the final pair T.  Every threshold ever used or
+// compacted to is >= T, so every stream buffer holds all of its stream's columns with
+// (key, id) <= T, for any column order:
+//   * exact mode (alpha100 = 0): a stream compacts to >= L of its own entries, so >= L entries
+//     lie at or below T and the union of the four buffers contains the row's exact top-L;
+//   * extrapolated mode: a stream compacts to rank ~ alpha * (L/NS) * (fraction seen) + beta;
+//     the row is exact iff the union holds >= L entries at or below T, else it is listed for
+//     the fallback launch (knn_tc.cu: knn_core).
+//
+// Roles (persistent, one CTA per SM, 10 warps):
+//   warp 0: TMA producer — the RB-row resident block (K atoms of RB x 128 B, 128B swizzle, plus
+//           a 32B-swizzle K-tail atom), then 128-column tiles through a ring of 16 KB slots;
+//   warp 1: TMEM allocator (512 columns = NBUF buffers of RB) + single-thread MMA issuer;
+//   warps 2..9: epilogue; warp (q = warp % 4, a) reads TMEM lanes 32q.. (stream q) for rows
+//           a*RB/2 .. a*RB/2 + RB/2 - 1, 32 rows per tcgen05.ld.
+#include "knn_common.cuh"
+
+namespace sg {
+namespace {
+
+constexpr uint32_t NS = 4;                // candidate streams per row (TMEM lane quadrants)
+constexpr uint32_t T_SORT = 512;          // union / sort buffer entries per warp
+constexpr uint32_t T_SCR = T_SORT * 8 + 128;   // per-warp scratch: sort buffer (aliased by select_L's
+                                               // histogram and the staged chunk) + 32 staged masks
+constexpr float FLT_BIG = 3.40282347e38f; // initial threshold: every finite key passes, +inf padding not
+
+struct TState {                           // per CTA, shared memory: selection state
+    unsigned long long pair[BM];          // row threshold (ord(key) << 32 | id), lowered by atomicMin
+    float key[BM];                        // its key as float for the ballot test (may lag: only larger)
+    uint32_t cnt[NS][BM];                 // candidates per (stream, row)
+};
+
+template <int KIND>
+__host__ __device__ constexpr uint32_t instr_desc_t(uint32_t n) {
+    // D fp32; A (M side, streamed columns) and B (N side, resident rows) f16 or tf32, K-major
+    return (1u << 4) | ((KIND ? 2u : 0u) << 7) | ((KIND ? 2u : 0u) << 10) | ((n >> 3) << 17) | ((MSUB >> 4) << 24);
+}
+
+__device__ __forceinline__ uint64_t pair_ord(float key, uint32_t id) { return ((uint64_t)f2ord(key) << 32) | id; }
+
+// Compaction of one stream buffer rb[0..cnt) (raw words) under the row threshold pair `cap`:
+// entries above `cap` are dropped; of the rest, if more than keep_max remain, only those with key
+// <= T are kept, T found by bit descent on the ordered key (count(key <= T) >= want, stopping as
+// soon as it is <= keep_max, else the smallest such T; ties on T are never split).  Returns the
+// new threshold pair (T, SENT), or `cap` when nothing had to be selected.  All lanes call.
+template <int EPL>
+__device__ __forceinline__ uint64_t select_pairs(uint64_t* rb, uint32_t cnt, uint64_t cap, uint32_t want,
+                                                 uint32_t keep_max, uint32_t lane, uint32_t* kept) {
+    uint64_t e[EPL];
+    uint32_t k[EPL];
+    uint32_t n = 0;
+#pragma unroll
+    for (int i = 0; i < EPL; i++) {
+        const uint32_t idx = i * 32 + lane;
+        e[i] = idx < cnt ? rb[idx] : 0ull;
+        const uint64_t po = raw2ord(e[i]);
+        const bool in = idx < cnt && po <= cap;
+        k[i] = in ? (uint32_t)(po >> 32) : 0xFFFFFFFFu;
+        n += __popc(__ballot_sync(0xffffffffu, in));
+    }
+    uint64_t P = cap;
+    uint32_t T = 0xFFFFFFFEu;                   // keep every entry at or below cap
+    if (n > keep_max && n > want) {
+        uint32_t lo = 0xFFFFFFFFu, hi = 0;
+#pragma unroll
+        for (int i = 0; i < EPL; i++)
+            if (k[i] != 0xFFFFFFFFu) { lo = min(lo, k[i]); hi = max(hi, k[i]); }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        T = hi;
+        if (lo != hi) {
+            int b = 31 - __clz(lo ^ hi);
+            uint32_t pfx = b >= 31 ? 0u : lo & ~((2u << b) - 1u);
+            bool done = false;
+#pragma unroll 1
+            for (; b >= 0; b--) {
+                const uint32_t t = pfx | ((1u << b) - 1u);
+                uint32_t c = 0;
+#pragma unroll
+                for (int i = 0; i < EPL; i++) c += __popc(__ballot_sync(0xffffffffu, k[i] <= t));
+                if (c >= want) {
+                    T = t;
+                    if (c <= keep_max) { done = true; break; }
+                } else {
+                    pfx |= 1u << b;
+                }
+            }
+            if (!done) T = pfx;
+        }
+        const uint64_t PT = ((uint64_t)T << 32) | SG_SENT;
+        P = PT < cap ? PT : cap;
+    }
+    uint32_t base = 0;
+#pragma unroll
+    for (int i = 0; i < EPL; i++) {
+        const bool sel = k[i] <= T;
+        const uint32_t bal = __ballot_sync(0xffffffffu, sel);
+        if (sel) rb[base + __popc(bal & ((1u << lane) - 1u))] = e[i];
+        base += __popc(bal);
+    }
+    __syncwarp();
+    *kept = base;
+    return P;
+}
+
+template <int KIND, int NKA, int MINI, int CS>
+__global__ void __launch_bounds__(NTHREADS, 1)
+knn_tct_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+               const __grid_constant__ CUtensorMap tmAm, const __grid_constant__ CUtensorMap tmBm, KnnParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    constexpr uint32_t EL = KIND ? 4 : 2;
+    constexpr uint32_t ATOM_K = 128 / EL;                  // elements per 128-byte atom
+    constexpr uint32_t NSLOT = NKA + MINI;                 // ring slots per column tile
+    constexpr uint32_t RB = KIND == 0 ? 256 : 128;         // resident rows = MMA N
+    constexpr uint32_t NHALF = RB / MSUB;                  // 128-row TMA boxes per atom
+    constexpr uint32_t NBUF = 512 / RB;                    // TMEM accumulator buffers
+    constexpr uint32_t RW = RB / 2;                        // rows per epilogue warp (sweep)
+    constexpr uint32_t NCH = RW / 32;                      // 32-row chunks per warp and tile
+    constexpr uint32_t FR = RW / 4;                        // rows per warp in the final phase
+    constexpr uint32_t AATOM = RB * 128;                   // resident bytes per K atom
+    constexpr uint32_t ABYTES = NKA * AATOM + (MINI ? RB * 32 : 0u);
+    constexpr uint32_t EPLC = CS / 32;                     // buffer entries per lane (compaction)
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + ABYTES;
+    Bars* bars = (Bars*)(sB + p.stages * SLOT);
+    uint8_t* bars_end = (uint8_t*)(bars + 1);
+    TState* ts = (TState*)(bars_end + ((128u - (smem_u32(bars_end) & 127u)) & 127u));   // float4 reads
+    uint8_t* ts_end = (uint8_t*)(ts + 1);
+    uint8_t* scratch_all = ts_end + ((128u - (smem_u32(ts_end) & 127u)) & 127u);
+
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t ma = p.n_rows_dev ? *(const volatile uint32_t*)p.n_rows_dev : p.ma;
+    const uint32_t n_rb = (ma + RB - 1) / RB;
+
+    if (threadIdx.x == 0) {
+        for (uint32_t s = 0; s < p.stages; s++) { mbar_init(&bars->full[s], 1); mbar_init(&bars->empty[s], 1); }
+        mbar_init(&bars->a_full, 1);
+        mbar_init(&bars->a_empty, 1);
+        for (uint32_t b = 0; b < NBUF_MAX; b++) { mbar_init(&bars->tm_full[b], 1); mbar_init(&bars->tm_empty[b], NEPI); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmA) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmB) : "memory");
+        if (MINI) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmAm) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmBm) : "memory");
+        }
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&bars->tmem_base)),
+                     "r"(512u));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = bars->tmem_base;
+
+    if (warp == 0) {
+        // ===================== TMA producer =====================
+        if (lane == 0) {
+            uint32_t stage = 0, sph = 0, it = 0;
+            for (uint32_t rb = blockIdx.x; rb < n_rb; rb += gridDim.x, it++) {
+                if (it > 0) mbar_wait(&bars->a_empty, (it - 1) & 1);
+                mbar_expect_tx(&bars->a_full, ABYTES);
+                for (uint32_t h = 0; h < NHALF; h++) {
+                    for (int ka = 0; ka < NKA; ka++)
+                        tma_load_2d(&tmA, &bars->a_full, sA + ka * AATOM + h * ATOM, ka * ATOM_K, rb * RB + h * MSUB);
+                    if (MINI) tma_load_2d(&tmAm, &bars->a_full, sA + NKA * AATOM + h * MINIB, NKA * ATOM_K, rb * RB + h * MSUB);
+                }
+                for (uint32_t ti = 0, t = tile_at(p, rb, 0); ti < p.n_ct; ti++, t = t + 1 == p.n_ct ? 0 : t + 1) {
+#pragma unroll
+                    for (uint32_t ka = 0; ka < NSLOT; ka++) {
+                        mbar_wait(&bars->empty[stage], sph ^ 1);
+                        if (ka < NKA) {
+                            mbar_expect_tx(&bars->full[stage], BATOM);
+                            tma_load_2d(&tmB, &bars->full[stage], sB + stage * SLOT, ka * ATOM_K, t * BN);
+                        } else {
+                            mbar_expect_tx(&bars->full[stage], BMINI);
+                            tma_load_2d(&tmBm, &bars->full[stage], sB + stage * SLOT, NKA * ATOM_K, t * BN);
+                        }
+                        if (++stage == p.stages) { stage = 0; sph ^= 1; }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer: D[column j][row i] =====================
+        if (lane == 0) {
+            constexpr uint32_t idesc = instr_desc_t<KIND>(RB);
+            const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
+            uint32_t stage = 0, sph = 0, it = 0, git = 0;
+            for (uint32_t rb = blockIdx.x; rb < n_rb; rb += gridDim.x, it++) {
+                mbar_wait(&bars->a_full, it & 1);
+                tc_fence_after();
+                for (uint32_t ti = 0; ti < p.n_ct; ti++, git++) {
+                    const uint32_t buf = git % NBUF;
+                    mbar_wait(&bars->tm_empty[buf], ((git / NBUF) & 1) ^ 1);
+                    tc_fence_after();
+                    const uint32_t dcol = tmem + buf * RB;
+#pragma unroll
+                    for (uint32_t ka = 0; ka < NSLOT; ka++) {
+                        mbar_wait(&bars->full[stage], sph);
+                        tc_fence_after();
+                        const uint32_t bslot = b_base + stage * SLOT;
+                        if (ka < NKA) {
+#pragma unroll
+                            for (uint32_t kk = 0; kk < 4; kk++)
+                                tc_mma<KIND>(dcol, desc_sw128(bslot + kk * 32), desc_sw128(a_base + ka * AATOM + kk * 32),
+                                             idesc, (ka | kk) != 0);
+                        } else {
+                            tc_mma<KIND>(dcol, desc_sw32(bslot), desc_sw32(a_base + NKA * AATOM), idesc, NKA != 0);
+                        }
+                        tc_commit(&bars->empty[stage]);
+                        if (++stage == p.stages) { stage = 0; sph ^= 1; }
+                    }
+                    tc_commit(&bars->tm_full[buf]);
+                }
+                tc_commit(&bars->a_empty);
+            }
+        }
+    } else {
+        // ===================== epilogue: ballot selection =====================
+        const uint32_t e = warp - 2, q = warp & 3, a = e >> 2;
+        const uint32_t row0 = a * RW;                        // first resident row of this warp
+        uint64_t* sortbuf = (uint64_t*)(scratch_all + e * T_SCR);
+        uint32_t* hist = (uint32_t*)sortbuf;
+        uint32_t* stage = (uint32_t*)sortbuf;                // 32 x 32 staged keys (sweep only)
+        uint4* smsk = (uint4*)(scratch_all + e * T_SCR + 4096);   // 32 staged row masks
+        const uint32_t tl = tmem + ((q * 32) << 16);
+        const uint32_t lt = (1u << lane) - 1u;
+        // buffer of (row R of the block, stream s): C words
+        auto rowbuf = [&](uint32_t R, uint32_t s) -> uint64_t* {
+            return p.cand + (((uint64_t)blockIdx.x * BM + R) * NS + s) * CS;
+        };
+        uint32_t git = 0;
+        for (uint32_t rb = blockIdx.x; rb < n_rb; rb += gridDim.x) {
+#pragma unroll
+            for (uint32_t k = 0; k < NCH; k++) {
+                const uint32_t R = row0 + 32 * k + lane;
+                const bool valid = rb * RB + R < ma;
+                if (q == 0) {   // row state: one writer; the barrier below publishes it
+                    ts->key[R] = valid ? FLT_BIG : -__int_as_float(0x7f800000);
+                    ts->pair[R] = valid ? pair_ord(FLT_BIG, SG_SENT) : 0ull;
+                }
+                ts->cnt[q][R] = 0;
+            }
+            named_bar_sync(1 + a, 128);
+            for (uint32_t ti = 0, t = tile_at(p, rb, 0); ti < p.n_ct; ti++, git++, t = t + 1 == p.n_ct ? 0 : t + 1) {
+                const uint32_t buf = git % NBUF;
+                const uint32_t col = t * BN + q * 32 + lane;  // this lane's column (operand order)
+                const uint32_t idv = p.col_map ? __ldg(p.col_map + col) : col;
+                // the row block's own columns (self exclusion) lie in this tile only near the diagonal
+                const bool self_tile = p.self_exclude && (p.self_col || (t * BN < rb * RB + RB && rb * RB < t * BN + BN));
+                mbar_wait(&bars->tm_full[buf], (git / NBUF) & 1);
+                tc_fence_after();
+#pragma unroll 1
+                for (uint32_t k = 0; k < NCH; k++) {
+                    const uint32_t Rb = row0 + 32 * k;        // first row of the chunk
+                    uint32_t v[32];
+                    tmem_ld32_nowait(tl + buf * RB + Rb, v);
+                    tmem_wait_ld();
+                    if (k == NCH - 1) {
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&bars->tm_empty[buf]);
+                    }
+                    if (p.noepi) {
+                        if ((v[0] ^ v[31]) == 0x7fc00001u) p.out_ids[0] = v[1];   // keep the loads live
+                        continue;
+                    }
+                    if (p.probe) {
+                        const uint32_t rowg = rb * RB + Rb;
+#pragma unroll
+                        for (int r = 0; r < 32; r++)
+                            if (rowg + r < ma && col < p.mb) p.probe[(uint64_t)(rowg + r) * p.mb + col] = __uint_as_float(v[r]);
+                        continue;
+                    }
+                    // candidate masks: bit c of msk[r] = column (32q + c) passes row Rb + r
+                    float th[32];
+                    const float4* th4 = (const float4*)&ts->key[Rb];
+#pragma unroll
+                    for (int g = 0; g < 8; g++) {
+                        const float4 t4 = th4[g];
+                        th[4 * g] = t4.x; th[4 * g + 1] = t4.y; th[4 * g + 2] = t4.z; th[4 * g + 3] = t4.w;
+                    }
+                    uint32_t msk[32], any = 0;
+#pragma unroll
+                    for (int r = 0; r < 32; r++) {
+                        msk[r] = __ballot_sync(0xffffffffu, __uint_as_float(v[r]) <= th[r]);
+                        any |= msk[r];
+                    }
+                    if (p.abl & 1) any = 0;
+                    if (any == 0) continue;
+                    uint32_t cntv = ts->cnt[q][Rb + lane];   // this lane holds the count of row Rb + lane
+                    // stage the chunk (keys [row][column], masks) so that the rows with candidates
+                    // are handled by one compact loop (32 inlined row blocks thrash the i-cache)
+#pragma unroll
+                    for (int r = 0; r < 32; r++) stage[r * 32 + lane] = v[r];
+                    if (lane == 0) {
+#pragma unroll
+                        for (int g = 0; g < 8; g++)
+                            smsk[g] = make_uint4(msk[4 * g], msk[4 * g + 1], msk[4 * g + 2], msk[4 * g + 3]);
+                    }
+                    __syncwarp();
+                    uint32_t rows = __ballot_sync(0xffffffffu, ((const uint32_t*)smsk)[lane] != 0);
+                    // the insertion test is inclusive (key <= thr): ties with a split threshold pair
+                    // may enter with a larger id, which only adds entries above the pair (dropped
+                    // at the next compaction / ignored by the final check)
+                    uint64_t* wb = rowbuf(Rb, q);
+                    while (rows) {
+                        const uint32_t r = __ffs(rows) - 1;
+                        rows &= rows - 1;
+                        uint32_t mr = ((const uint32_t*)smsk)[r];
+                        const uint32_t kb = stage[r * 32 + lane];
+                        if (self_tile) {
+                            const uint32_t rowg = rb * RB + Rb + r;
+                            const uint32_t sc = p.self_col ? (rowg < ma ? __ldg(p.self_col + rowg) : SG_SENT) : rowg;
+                            mr = __ballot_sync(0xffffffffu, ((mr >> lane) & 1u) && col != sc);
+                        }
+                        const uint32_t base = __shfl_sync(0xffffffffu, cntv, r);
+                        if ((mr >> lane) & 1u) wb[(uint64_t)r * (NS * CS) + base + __popc(mr & lt)] = ((uint64_t)kb << 32) | idv;
+                        if (lane == r) cntv += __popc(mr);
+                    }
+                    // compaction: rows whose stream buffer cannot take another 32 columns, and (in
+                    // extrapolated mode) eagerly once a stream holds EAGER entries above its target
+                    // rank, so that the row threshold follows the fraction of columns seen
+                    uint32_t want = p.L, kmax = p.L + (CS - 32 - p.L) / 8;
+                    if (p.alpha100) {
+                        const uint64_t rr = (uint64_t)p.alpha100 * p.L * (ti + 1) / (100ull * NS * p.n_ct) + p.beta;
+                        const uint32_t cap = (CS - 32) / 2;
+                        want = (uint32_t)(rr < cap ? rr : cap);
+                        if (want > p.L) want = p.L;
+                        kmax = want + (CS - 32 - want) / 8;
+                    }
+                    const uint32_t trig = p.alpha100 ? min(CS - 32, want + p.eager) : CS - 32;
+                    uint32_t need = __ballot_sync(0xffffffffu, cntv > trig);
+                    if (need) {
+                        do {
+                            const int o = __ffs(need) - 1;
+                            need &= need - 1;
+                            const uint32_t c_o = __shfl_sync(0xffffffffu, cntv, o);
+                            const uint32_t R = Rb + o;
+                            uint64_t* ob = rowbuf(R, q);
+                            uint32_t kept;
+                            const uint64_t cur = *(volatile unsigned long long*)&ts->pair[R];
+                            uint64_t P = select_pairs<EPLC>(ob, c_o, cur, want, kmax, lane, &kept);
+                            if (kept > CS - 32) {   // massive ties on the threshold key: split them by id
+                                P = select_L<EPLC>(ob, kept, want, kmax, hist, lane, &kept);
+                            }
+                            if (lane == (uint32_t)o) {
+                                cntv = kept;
+                                if (P < atomicMin(&ts->pair[R], (unsigned long long)P)) ts->key[R] = ord2f((uint32_t)(P >> 32));
+                            }
+                        } while (need);
+                    }
+                    ts->cnt[q][Rb + lane] = cntv;
+                    __syncwarp();
+                }
+            }
+            if (p.probe || p.noepi) continue;
+            // ---- final: union of the row's NS stream buffers, exactness check, sorted top-L
+            named_bar_sync(1 + a, 128);   // the four stream warps of this half are done
+            for (uint32_t o = 0; o < FR; o++) {
+                const uint32_t R = row0 + q * FR + o;
+                const uint32_t rowg = rb * RB + R;
+                if (rowg >= ma) continue;
+                const uint64_t tmin = ts->pair[R];
+                uint32_t c[NS], total = 0;
+#pragma unroll
+                for (uint32_t s = 0; s < NS; s++) {
+                    c[s] = ts->cnt[s][R];
+                    if (c[s] > p.L) {   // a stream's own top-L holds all its entries of the row's top-L
+                        uint64_t* sb = rowbuf(R, s);
+                        uint32_t kept;
+                        select_pairs<EPLC>(sb, c[s], tmin, p.L, p.L, lane, &kept);
+                        if (kept > T_SORT / NS) {
+                            select_L<EPLC>(sb, kept, p.L, p.L, hist, lane, &kept);
+                            kept = p.L;
+                        }
+                        c[s] = kept;
+                    }
+                }
+#pragma unroll
+                for (uint32_t s = 0; s < NS; s++) {
+                    const uint64_t* sb = rowbuf(R, s);
+                    for (uint32_t i = lane; i < c[s]; i += 32) sortbuf[total + i] = sb[i];
+                    total += c[s];
+                }
+                __syncwarp();
+                if (p.alpha100 && tmin != pair_ord(FLT_BIG, SG_SENT)) {
+                    // exact iff >= L union entries lie at or below every stream's threshold pair
+                    uint32_t n_le = 0;
+                    for (uint32_t i0 = 0; i0 < total; i0 += 32) {
+                        const uint32_t i = i0 + lane;
+                        n_le += __popc(__ballot_sync(0xffffffffu, i < total && raw2ord(sortbuf[i]) <= tmin));
+                    }
+                    if (n_le < p.L) {
+                        if (lane == 0) p.fail_rows[atomicAdd(p.fail_count, 1u)] = rowg;
+                        __syncwarp();
+                        continue;
+                    }
+                }
+                if (total > p.L) {
+                    uint32_t kept;
+                    select_keys<T_SORT / 32>(sortbuf, total, p.L, p.L, lane, &kept);
+                    total = kept;
+                }
+                const uint64_t orow = p.row_map ? p.row_map[rowg] : rowg;
+                finish_row(sortbuf, total, sortbuf, 0, p.L, sortbuf, p.norm_a[rowg], p.out_ids + orow * p.L,
+                           p.out_d + orow * p.L, lane);
+            }
+            named_bar_sync(1 + a, 128);   // buffers and state are reused by the next row block
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u));
+    }
+}
+
+template <int KIND, int NKA, int MINI, int CS>
+sg_status launch_tt(const CUtensorMap* maps, KnnParams& p, cudaStream_t st) {
+    constexpr uint32_t RB = KIND == 0 ? 256 : 128;
+    constexpr uint32_t ABYTES = NKA * RB * 128 + (MINI ? RB * 32 : 0u);
+    const size_t fixed = ABYTES + sizeof(Bars) + 128 + sizeof(TState) + 128 + NEPI * T_SCR + 1024 + 64;
+    const size_t budget = 227 * 1024;
+    if (fixed + (NKA + MINI) * SLOT > budget) { set_error("kNN: operand too wide for shared memory"); return SG_ERR_UNSUPPORTED; }
+    uint32_t stages = (uint32_t)((budget - fixed) / SLOT);
+    if (stages > MAX_STAGES) stages = MAX_STAGES;
+    p.stages = stages;
+    const size_t smem = fixed + stages * SLOT;
+    auto kern = knn_tct_kernel<KIND, NKA, MINI, CS>;
+    SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const uint32_t grid = p.n_rb < (uint32_t)num_sms() ? p.n_rb : (uint32_t)num_sms();
+    knn_time_begin(st);
+    kern<<<grid, NTHREADS, smem, st>>>(maps[0], maps[1], maps[2], maps[3], p);
+    SG_LAUNCHED("knn_tct_kernel");
+    knn_time_end(st);
+    return SG_OK;
+}
+
+template <int KIND, int MINI, int CS>
+sg_status launch_tt_nka(int nka, const CUtensorMap* maps, KnnParams& p, cudaStream_t st) {
+    switch (nka) {
+        case 1: return launch_tt<KIND, 1, MINI, CS>(maps, p, st);
+        case 2: return launch_tt<KIND, 2, MINI, CS>(maps, p, st);
+        case 3: return launch_tt<KIND, 3, MINI, CS>(maps, p, st);
+        case 4: return launch_tt<KIND, 4, MINI, CS>(maps, p, st);
+    }
+    set_error("kNN: unsupported operand width (%d atoms)", nka);
+    return SG_ERR_UNSUPPORTED;
+}
+
+template <int KIND, int CS>
+sg_status launch_tt_mini(int nka, int mini, const CUtensorMap* maps, KnnParams& p, cudaStream_t st) {
+    return mini ? launch_tt_nka<KIND, 1, CS>(nka, maps, p, st) : launch_tt_nka<KIND, 0, CS>(nka, maps, p, st);
+}
+
+}  // namespace
+
+// Buffer words per (row, stream): extrapolated mode keeps few per stream; exact mode >= L + 32.
+uint32_t knn_t_cap(uint32_t L, bool extrap) { return extrap || L + 64 <= 128 ? 128u : 256u; }
+
+sg_status launch_knn_t(const CUtensorMap* maps, KnnParams& p, int esize, int nka, int mini, cudaStream_t st) {
+    if (p.C == 128) return esize == 4 ? launch_tt_mini<1, 128>(nka, mini, maps, p, st) : launch_tt_mini<0, 128>(nka, mini, maps, p, st);
+    return esize == 4 ? launch_tt_mini<1, 256>(nka, mini, maps, p, st) : launch_tt_mini<0, 256>(nka, mini, maps, p, st);
+}
+
+}  // namespace sg

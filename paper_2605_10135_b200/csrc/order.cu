@@ -51,6 +51,12 @@ static uint64_t group_rows() {
 }
 
 uint32_t order_groups(uint64_t m) {
+    // Off by default: with the extrapolated thresholds of the distance kernel (knn_tc.cu) the
+    // columns must arrive in an order unrelated to the row's position, which the plain id order
+    // is; the spatial order + rotated sweep remains available for comparison.
+    static int on = -1;
+    if (on < 0) { const char* e = getenv("SG_KNN_ORDER"); on = e ? atoi(e) : 0; }
+    if (!on) return 0;
     uint64_t kc = m / group_rows();
     if (kc > 8192) kc = 8192;
     return (uint32_t)kc;
@@ -66,7 +72,7 @@ size_t order_workspace(uint64_t m, uint32_t d, int prec, int metric) {
     cv.take<uint32_t>(kc);          // fill
     cv.take<uint64_t>(kc + 1);      // offsets
     return cv.off + operand_bytes(prec, metric, d, m, SIDE_A) + operand_bytes(prec, metric, d, kc, SIDE_B) +
-           knn_core_workspace(1) + scan_workspace(kc) + 4096;
+           knn_core_workspace(1, m, d, prec, metric) + scan_workspace(kc) + 4096;
 }
 
 sg_status spatial_order(const void* x, sg_dtype dtype, uint32_t d, const uint32_t* idmap, uint64_t m, int prec,
