@@ -68,6 +68,24 @@ def lpt_owner(sizes, world):
     return owner
 
 
+def broadcast_centroids(C: torch.Tensor, world: int) -> torch.Tensor:
+    """N1: rank 0's k x d centroids to every rank (in place; NCCL over NVLink on GPUs)."""
+    if world > 1:
+        dist.broadcast(C, src=0)
+    return C
+
+
+def exchange_records(sendbuf: torch.Tensor, send: list, recv: list, W: int) -> torch.Tensor:
+    """N2: all-to-all of the merge records (W int32 words each).  `send[r]` / `recv[r]` count the
+    records this rank sends to / receives from rank r (both known locally from `home`, so no count
+    exchange is needed); records arrive grouped by source rank, in rank order."""
+    nrecv = sum(recv)
+    recvbuf = torch.empty(max(nrecv, 1) * W, dtype=torch.int32, device=sendbuf.device)
+    dist.all_to_all_single(recvbuf[: nrecv * W], sendbuf[: sum(send) * W], [c * W for c in recv],
+                           [c * W for c in send])
+    return recvbuf
+
+
 class _Timer:
     def __init__(self, on: bool):
         self.on = on
@@ -99,8 +117,7 @@ def build_index(x: torch.Tensor, cfg: BuildConfig, rank: int = 0, world: int = 1
         C = api.scalegann_kmeans(x, cfg.k, seed=cfg.kmeans_seed, max_iter=cfg.kmeans_iters, spc=cfg.kmeans_spc, ws=ws)
     else:
         C = torch.empty(cfg.k, d, dtype=torch.float32, device=x.device)
-    if world > 1:
-        dist.broadcast(C, src=0)
+    broadcast_centroids(C, world)
     # a2-a3 — partition (identical on every rank)
     tm.mark("a2a3_partition")
     home, pd, counts = api.scalegann_partition(x, C, omega=cfg.omega, epsilon=cfg.epsilon,
@@ -132,8 +149,7 @@ def build_index(x: torch.Tensor, cfg: BuildConfig, rank: int = 0, world: int = 1
             graphs = [torch.empty(0, R, dtype=torch.int32, device=x.device) if s == 0 else None
                       for s in range(cfg.k)]
         sendbuf = api.scalegann_merge_pack(home, inv, owner, rank, world, idmaps, graphs, graphs_d, sum(send), ws=ws)
-        recvbuf = torch.empty(max(sum(recv), 1) * W, dtype=torch.int32, device=x.device)
-        dist.all_to_all_single(recvbuf[: sum(recv) * W], sendbuf, [c * W for c in recv], [c * W for c in send])
+        recvbuf = exchange_records(sendbuf, send, recv, W)
         merged, merged_d = api.scalegann_merge_union(home, inv, owner, rank, idmaps, graphs, graphs_d, recvbuf,
                                                      sum(recv), ws=ws)
     tm.mark("end")
