@@ -1,11 +1,11 @@
 // a6 — rank-based detour-count prune (north_star stage 3; reading R10, CAGRA prior art).
 //
-// One warp per node a.  N[a] (L ids) goes into a shared-memory open-addressing table
-// id -> rank.  For each rank r_ad the warp reads the 2-hop row N[delta] (delta = N[a][r_ad])
+// One warp per node a.  N[a] (L ids) goes into a shared-memory bucketized table id -> rank
+// (L/2 buckets of 8 slots + stash: a lookup is two 16-byte loads and 8 compares, no probing).  For each rank r_ad the warp reads the 2-hop row N[delta] (delta = N[a][r_ad])
 // with coalesced 16-byte loads (4 rows in flight per lane batch) and, for every b in it that
 // is also in N[a] at rank r_ab with max(r_ad, r_db) < r_ab (rule P; rule 1: r_ad < r_ab),
-// increments cnt[r_ab] in shared memory.  The ranks are then bitonic-sorted by
-// (cnt, rank) (sentinel ranks last) and the first R written with their kNN distances.
+// increments cnt[r_ab] in shared memory.  The ranks are then ordered stably by (cnt, rank)
+// (sentinel ranks last) with a counting sort and the first R written with their kNN distances.
 // Bit-exact with the oracle (integer work only).
 #include "common.cuh"
 
@@ -15,79 +15,230 @@ namespace {
 
 __device__ __forceinline__ uint32_t hslot(uint32_t id, uint32_t bits) { return (id * 0x9E3779B1u) >> (32 - bits); }
 
+// Membership table of N[a]: NB = LP/2 buckets of 8 slots (keys u32, ranks u8), one hash; a
+// lookup reads the whole bucket with two 16-byte loads and compares 8 keys, with no probe loop (a
+// probing table makes every lane wait for the warp's longest chain).  Keys that find their
+// bucket full go to a small stash, scanned only when it is not empty (warp-uniform).
+constexpr uint32_t STASH = 32;
+constexpr uint32_t EMPTY = 0xFFFFFFFEu;   // empty slot: no id (< 2^31) and not SENT, so never matched
+
+template <uint32_t NB, uint32_t NBB>
+__device__ __forceinline__ uint32_t lookup(const uint4* bk, const uint2* br, const uint32_t* sk, const uint8_t* sr,
+                                           uint32_t nstash, uint32_t b) {
+    const uint32_t h = hslot(b, NBB);
+    const uint4 k0 = bk[2 * h], k1 = bk[2 * h + 1];
+    const uint2 rw = br[h];
+    uint32_t r = 0xFFFFFFFFu;
+    r = k0.x == b ? (rw.x & 0xFFu) : r;
+    r = k0.y == b ? ((rw.x >> 8) & 0xFFu) : r;
+    r = k0.z == b ? ((rw.x >> 16) & 0xFFu) : r;
+    r = k0.w == b ? (rw.x >> 24) : r;
+    r = k1.x == b ? (rw.y & 0xFFu) : r;
+    r = k1.y == b ? ((rw.y >> 8) & 0xFFu) : r;
+    r = k1.z == b ? ((rw.y >> 16) & 0xFFu) : r;
+    r = k1.w == b ? (rw.y >> 24) : r;
+    if (nstash) {
+        for (uint32_t i = 0; i < nstash; i++) r = sk[i] == b ? sr[i] : r;
+    }
+    return r;
+}
+
+constexpr uint32_t QCAP = 256;   // lookup queue entries per warp (flushed every 256 / (32 LPL) rows)
+
+template <int LPL>
+__device__ __forceinline__ void load_rows(const uint32_t* __restrict__ knn, const uint32_t* na, uint32_t r0, uint32_t L,
+                                          uint32_t lane, uint32_t (&bv)[4][LPL]) {
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+        const uint32_t dl = r0 + u < L ? na[r0 + u] : SG_SENT;
+#pragma unroll
+        for (int q = 0; q < LPL; q++) {
+            const uint32_t rdb = q * 32 + lane;
+            bv[u][q] = (dl != SG_SENT && rdb < L) ? __ldg(knn + (uint64_t)dl * L + rdb) : SG_SENT;
+        }
+    }
+}
+
 template <int LPL, int PW>   // ranks per lane = L_pad / 32; warps (nodes) per CTA
 __global__ void __launch_bounds__(PW * 32) prune_kernel(const uint32_t* __restrict__ knn, const float* __restrict__ knn_d,
                                                         uint64_t m, uint32_t L, uint32_t R, uint32_t rule,
                                                         uint32_t* __restrict__ out, float* __restrict__ out_d) {
     constexpr uint32_t LP = LPL * 32;          // padded L (power of two)
-    constexpr uint32_t HS = 2 * LP;            // hash slots
-    constexpr uint32_t HB = LPL == 1 ? 6 : LPL == 2 ? 7 : LPL == 4 ? 8 : 9;
-    __shared__ uint32_t s_key[PW][HS];
-    __shared__ uint16_t s_rank[PW][HS];
-    __shared__ uint32_t s_cnt[PW][LP];
-    __shared__ uint32_t s_na[PW][LP];
-    __shared__ uint64_t s_sort[PW][LP];
+    constexpr uint32_t NB = LP / 2;            // buckets of 8 slots: load factor 1/4
+    constexpr uint32_t NBB = LPL == 1 ? 4 : LPL == 2 ? 5 : LPL == 4 ? 6 : 7;
+    constexpr uint32_t FLUSH = QCAP / (32 * LPL) < 4 ? QCAP / (32 * LPL) : 4;   // rows per queue flush
+    static_assert((1u << NBB) == NB, "bucket bits");
+    extern __shared__ __align__(16) uint8_t sm[];
     const uint32_t w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint32_t* hk = s_key[w];
-    uint16_t* hr = s_rank[w];
-    uint32_t* cnt = s_cnt[w];
-    uint32_t* na = s_na[w];
-    uint64_t* keys = s_sort[w];
+    const uint32_t lt = (1u << lane) - 1u;
+    constexpr size_t PER = NB * 32 + NB * 8 + NB * 4 + STASH * 4 + STASH + 16 + 128 + LP * 4 * 2 + (LP + 1) * 4 + QCAP * 5;
+    uint8_t* base = sm + (size_t)w * ((PER + 15) / 16 * 16);
+    uint32_t* bkeys = (uint32_t*)base;                 // [NB][8]
+    uint8_t* branks = base + NB * 32;                  // [NB][8]
+    uint32_t* bfill = (uint32_t*)(branks + NB * 8);    // [NB]
+    uint32_t* sk = bfill + NB;                         // stash keys
+    uint8_t* sr = (uint8_t*)(sk + STASH);              // stash ranks
+    uint32_t* nst = (uint32_t*)(((uintptr_t)(sr + STASH) + 15) & ~(uintptr_t)15);   // stash count
+    uint32_t* bloom = nst + 4;                         // 32 words
+    uint32_t* cnt = bloom + 32;                        // detour count per rank
+    uint32_t* na = cnt + LP;                           // N[a]
+    uint32_t* off = na + LP;                           // counting-sort offsets per count value (L + 1)
+    uint32_t* qb = off + LP + 1;                       // lookup queue: 2-hop ids
+    uint8_t* qm = (uint8_t*)(qb + QCAP);               // and their max(r_ad, r_db)
     const uint64_t nwarps = (uint64_t)gridDim.x * PW;
     for (uint64_t a = (uint64_t)blockIdx.x * PW + w; a < m; a += nwarps) {
         const uint32_t* Na = knn + a * L;
-        for (uint32_t i = lane; i < HS; i += 32) hk[i] = SG_SENT;
+        for (uint32_t i = lane; i < NB * 8; i += 32) bkeys[i] = EMPTY;
+        for (uint32_t i = lane; i < NB; i += 32) bfill[i] = 0;
+        if (lane == 0) *nst = 0;
         for (uint32_t r = lane; r < LP; r += 32) { na[r] = r < L ? Na[r] : SG_SENT; cnt[r] = 0; }
+        for (uint32_t r = lane; r <= LP; r += 32) off[r] = 0;
+        bloom[lane] = 0;
         __syncwarp();
         for (uint32_t r = lane; r < L; r += 32) {
             const uint32_t id = na[r];
             if (id == SG_SENT) continue;
-            uint32_t h = hslot(id, HB);
-            while (atomicCAS(&hk[h], SG_SENT, id) != SG_SENT) h = (h + 1) & (HS - 1);
-            hr[h] = (uint16_t)r;
+            const uint32_t h = hslot(id, NBB);
+            const uint32_t fb = (id * 0x9E3779B1u >> 10) & 1023u;
+            atomicOr(&bloom[fb >> 5], 1u << (fb & 31));
+            const uint32_t slot = atomicAdd(&bfill[h], 1u);
+            if (slot < 8) {
+                bkeys[h * 8 + slot] = id;
+                branks[h * 8 + slot] = (uint8_t)r;
+            } else {
+                const uint32_t i = atomicAdd(nst, 1u);
+                if (i < STASH) { sk[i] = id; sr[i] = (uint8_t)r; }
+            }
         }
         __syncwarp();
-        for (uint32_t r0 = 0; r0 < L; r0 += 4) {
-            uint32_t bv[4][LPL];
-            uint32_t dl[4];
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                dl[u] = r0 + u < L ? na[r0 + u] : SG_SENT;
-#pragma unroll
-                for (int q = 0; q < LPL; q++) {
-                    const uint32_t rdb = q * 32 + lane;
-                    bv[u][q] = (dl[u] != SG_SENT && rdb < L) ? __ldg(knn + (uint64_t)dl[u] * L + rdb) : SG_SENT;
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                const uint32_t r_ad = r0 + u;
-#pragma unroll
-                for (int q = 0; q < LPL; q++) {
-                    const uint32_t b = bv[u][q];
+        const uint32_t nstash = *nst;
+        const uint32_t fword = bloom[lane];   // 1024-bit membership filter, one word per lane
+        if (nstash > STASH) {   // pathological hash clustering: exact but slow path (never observed)
+            for (uint32_t r0 = 0; r0 < L; r0++) {
+                const uint32_t dl = na[r0];
+                if (dl == SG_SENT) continue;
+                for (uint32_t rdb = lane; rdb < L; rdb += 32) {
+                    const uint32_t b = __ldg(knn + (uint64_t)dl * L + rdb);
                     if (b == SG_SENT || b == (uint32_t)a) continue;
-                    const uint32_t r_db = q * 32 + lane;
-                    uint32_t h = hslot(b, HB), key;
-                    while ((key = hk[h]) != SG_SENT && key != b) h = (h + 1) & (HS - 1);
-                    if (key != b) continue;
-                    const uint32_t r_ab = hr[h];
-                    const uint32_t mx = rule == 0 ? max(r_ad, r_db) : r_ad;
-                    if (mx < r_ab) atomicAdd(&cnt[r_ab], 1u);
+                    const uint32_t mx = rule == 0 ? max(r0, rdb) : r0;
+                    for (uint32_t r = mx + 1; r < L; r++)
+                        if (na[r] == b) { atomicAdd(&cnt[r], 1u); break; }
                 }
+            }
+        } else {
+            // ~92% of 2-hop ids are not in N[a]: a register filter settles most of them; the rest
+            // are queued (ballot + prefix popc) and resolved densely against the table.  The next
+            // batch of 2-hop rows is loaded while the current one is filtered.
+            uint32_t bv[4][LPL], bn[4][LPL];
+            load_rows<LPL>(knn, na, 0, L, lane, bv);
+            for (uint32_t r0 = 0; r0 < L; r0 += 4) {
+                if (r0 + 4 < L) load_rows<LPL>(knn, na, r0 + 4, L, lane, bn);
+                uint32_t qn = 0;
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const uint32_t r_ad = r0 + u;
+#pragma unroll
+                    for (int q = 0; q < LPL; q++) {
+                        const uint32_t b = bv[u][q];
+                        const uint32_t r_db = q * 32 + lane;
+                        // only ranks r_ab > max(r_ad, r_db) (rule P) / > r_ad (rule 1) can count
+                        const uint32_t mx = rule == 0 ? max(r_ad, r_db) : r_ad;
+                        const uint32_t fb = (b * 0x9E3779B1u >> 10) & 1023u;
+                        const uint32_t fw = __shfl_sync(0xffffffffu, fword, fb >> 5);
+                        // SENT never matches a slot; a is not in N[a] (self excluded), so neither
+                        // needs a test here
+                        const bool pos = (fw >> (fb & 31)) & 1u;
+                        const uint32_t bal = __ballot_sync(0xffffffffu, pos);
+                        if (pos) {
+                            const uint32_t i = qn + __popc(bal & lt);
+                            qb[i] = b;
+                            qm[i] = (uint8_t)mx;
+                        }
+                        qn += __popc(bal);
+                    }
+                    if ((u + 1) % FLUSH == 0) {
+                        __syncwarp();
+                        for (uint32_t i = lane; i < qn; i += 32) {
+                            const uint32_t b = qb[i];
+                            const uint32_t r_ab = lookup<NB, NBB>((const uint4*)bkeys, (const uint2*)branks, sk, sr, nstash, b);
+                            if (r_ab != 0xFFFFFFFFu && qm[i] < r_ab) atomicAdd(&cnt[r_ab], 1u);
+                        }
+                        __syncwarp();
+                        qn = 0;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; u++)
+#pragma unroll
+                    for (int q = 0; q < LPL; q++) bv[u][q] = bn[u][q];
             }
         }
         __syncwarp();
-        for (uint32_t r = lane; r < LP; r += 32)
-            keys[r] = r >= L ? ~0ull : na[r] == SG_SENT ? ((0xFFFFFFFFull << 32) | r) : (((uint64_t)cnt[r] << 32) | r);
+        // stable counting sort of the ranks by detour count (sentinel ranks last): position of rank
+        // r = #{count < cnt[r]} + #{r' < r with the same count}; the first R are written
+        uint32_t cv[LPL];
+#pragma unroll
+        for (int i = 0; i < LPL; i++) {
+            const uint32_t r = i * 32 + lane;
+            cv[i] = r >= L ? 0xFFFFFFFFu : na[r] == SG_SENT ? L : cnt[r];   // counts are <= r < L
+            if (r < L) atomicAdd(&off[cv[i]], 1u);
+        }
         __syncwarp();
-        warp_sort_u64(keys, LP, lane);
-        for (uint32_t i = lane; i < R; i += 32) {
-            const uint32_t r = (uint32_t)keys[i];
-            out[a * R + i] = na[r];
-            out_d[a * R + i] = knn_d[a * L + r];
+        {   // exclusive scan of off[0..L]
+            uint32_t run = 0;
+            for (uint32_t c0 = 0; c0 <= L; c0 += 32) {
+                const uint32_t c = c0 + lane;
+                const uint32_t v = c <= L ? off[c] : 0;
+                uint32_t inc = v;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= (uint32_t)o) inc += t;
+                }
+                if (c <= L) off[c] = run + inc - v;
+                run += __shfl_sync(0xffffffffu, inc, 31);
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < LPL; i++) {   // rank groups in increasing rank order
+            const uint32_t r = i * 32 + lane;
+            const uint32_t c = cv[i];
+            const uint32_t grp = __match_any_sync(0xffffffffu, c);
+            const uint32_t leader = __ffs(grp) - 1;
+            uint32_t pos0 = 0;
+            if (lane == leader && c != 0xFFFFFFFFu) pos0 = atomicAdd(&off[c], __popc(grp));
+            const uint32_t pos = __shfl_sync(0xffffffffu, pos0, leader) + __popc(grp & lt);
+            if (c != 0xFFFFFFFFu && pos < R) {
+                out[a * R + pos] = na[r];
+                out_d[a * R + pos] = knn_d[a * L + r];
+            }
         }
         __syncwarp();
     }
+}
+
+template <int LPL, int PW>
+size_t prune_smem() {
+    constexpr uint32_t LP = LPL * 32, NB = LP / 2;
+    constexpr size_t PER = NB * 32 + NB * 8 + NB * 4 + STASH * 4 + STASH + 16 + 128 + LP * 4 * 2 + (LP + 1) * 4 + QCAP * 5;
+    return (size_t)PW * ((PER + 15) / 16 * 16) + 64;
+}
+
+template <int LPL, int PW>
+sg_status prune_launch(const uint32_t* knn, const float* knn_d, uint64_t m, uint32_t L, uint32_t R, uint32_t rule,
+                       uint32_t* out, float* out_d, cudaStream_t st) {
+    const size_t smem = prune_smem<LPL, PW>();
+    auto kern = prune_kernel<LPL, PW>;
+    SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PW * 32, smem));
+    if (per_sm < 1) per_sm = 1;
+    const uint64_t cap = (uint64_t)num_sms() * per_sm;
+    const uint64_t blocks = (m + PW - 1) / PW;
+    kern<<<(unsigned)(blocks < cap ? blocks : cap), PW * 32, smem, st>>>(knn, knn_d, m, L, R, rule, out, out_d);
+    SG_LAUNCHED("prune_kernel");
+    return SG_OK;
 }
 
 }  // namespace
@@ -95,14 +246,10 @@ __global__ void __launch_bounds__(PW * 32) prune_kernel(const uint32_t* __restri
 sg_status launch_prune(const uint32_t* knn, const float* knn_d, uint64_t m, uint32_t L, uint32_t R, uint32_t rule,
                        uint32_t* out, float* out_d, cudaStream_t st) {
     if (m == 0) return SG_OK;
-    const uint64_t cap = (uint64_t)num_sms() * 16;
-    auto grid = [&](int pw) { uint64_t b = (m + pw - 1) / pw; return (unsigned)(b < cap ? b : cap); };
-    if (L <= 32) prune_kernel<1, 8><<<grid(8), 8 * 32, 0, st>>>(knn, knn_d, m, L, R, rule, out, out_d);
-    else if (L <= 64) prune_kernel<2, 8><<<grid(8), 8 * 32, 0, st>>>(knn, knn_d, m, L, R, rule, out, out_d);
-    else if (L <= 128) prune_kernel<4, 8><<<grid(8), 8 * 32, 0, st>>>(knn, knn_d, m, L, R, rule, out, out_d);
-    else prune_kernel<8, 4><<<grid(4), 4 * 32, 0, st>>>(knn, knn_d, m, L, R, rule, out, out_d);
-    SG_LAUNCHED("prune_kernel");
-    return SG_OK;
+    if (L <= 32) return prune_launch<1, 8>(knn, knn_d, m, L, R, rule, out, out_d, st);
+    if (L <= 64) return prune_launch<2, 8>(knn, knn_d, m, L, R, rule, out, out_d, st);
+    if (L <= 128) return prune_launch<4, 8>(knn, knn_d, m, L, R, rule, out, out_d, st);
+    return prune_launch<8, 4>(knn, knn_d, m, L, R, rule, out, out_d, st);
 }
 
 }  // namespace sg
