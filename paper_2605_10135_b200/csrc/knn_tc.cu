@@ -221,116 +221,120 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 pw[0] += c1 - c0;
                 tc_fence_after();
                 const uint32_t tb = tl + buf * BN;
-#pragma unroll 1
-                for (uint32_t hp = 0; hp < BN / 32; hp++) {
-                    // 32 columns of the tile per pass (register budget: 10 warps x 168 registers);
-                    // the accumulator buffer is released once the last pass is in registers
-                    uint32_t v[32];
-                    if (p.noepi >= 3) {
+                // one 32-column pass (register budget: 10 warps x 168 registers)
+                auto pass = [&](uint32_t (&v)[32], const uint32_t hp) {
+                const uint32_t col0 = t * BN + hp * 32;
+                if (p.noepi) {
+                    if ((v[0] ^ v[31]) == 0x7fc00001u) p.out_ids[0] = v[1];   // keep the loads live
+                    c1 = clk();
+                    return;
+                }
+                if (p.probe) {
+                    if (valid) {
 #pragma unroll
-                        for (int j = 0; j < 32; j++) v[j] = 0;
-                    } else {
-                        tmem_ld32_nowait(tb + hp * 32, v);
+                        for (int j = 0; j < 32; j++)
+                            if (col0 + j < p.mb) p.probe[(uint64_t)row * p.mb + col0 + j] = __uint_as_float(v[j]);
                     }
+                    c1 = clk();
+                    return;
+                }
+                // reported id of this lane's column, fetched early (latency hidden by the mask)
+                const uint32_t id0 = p.col_map ? __ldg(p.col_map + col0 + lane) : col0 + lane;
+                c1 = clk();
+                // strict test when columns arrive in increasing id, inclusive with the rotated sweep
+                const float te = p.rotate ? next_up(thr) : thr;
+                uint32_t mq[4] = {0, 0, 0, 0};
+#pragma unroll
+                for (int s = 7; s >= 1; s -= 2) {
+#pragma unroll
+                    for (int g = 0; g < 4; g++) {
+                        const int j = g * 8 + s;
+                        uint32_t lo, hi;
+                        sub2(v[j - 1], v[j], te, lo, hi);
+                        mq[g] = __funnelshift_l(hi, mq[g], 1);
+                        mq[g] = __funnelshift_l(lo, mq[g], 1);
+                    }
+                }
+                uint32_t m = mq[0] | (mq[1] << 8) | (mq[2] << 16) | (mq[3] << 24);
+                // self column: row r of block rb is column rb*RB + r
+                if (scol - col0 < 32u) m &= ~(1u << (scol - col0));
+                c0 = clk();
+                pw[3] += c0 - c1;   // masks
+                if (p.abl & 1) m = 0;
+                if (__any_sync(0xffffffffu, m != 0)) {
+                    sids[lane] = id0;
+                    float4* st4 = (float4*)(skeys + lane * KSTRIDE);
+#pragma unroll
+                    for (int j4 = 0; j4 < 8; j4++)
+                        st4[j4] = make_float4(__uint_as_float(v[4 * j4]), __uint_as_float(v[4 * j4 + 1]),
+                                              __uint_as_float(v[4 * j4 + 2]), __uint_as_float(v[4 * j4 + 3]));
+                    __syncwarp();
+                    if constexpr (PROF) pw[6] += __popc(m);
+                    // two candidates per iteration: independent smem loads and global stores
+                    const float* mykeys = skeys + lane * KSTRIDE;
+                    while (m) {
+                        if constexpr (PROF) pw[7]++;
+                        const uint32_t b0 = 31 - __clz(m);
+                        m ^= 1u << b0;
+                        const bool two = m != 0;
+                        const uint32_t b1 = two ? 31 - __clz(m) : b0;
+                        m &= ~(1u << b1);
+                        const uint32_t k0 = __float_as_uint(mykeys[b0]), i0 = sids[b0];
+                        const uint32_t k1 = __float_as_uint(mykeys[b1]), i1 = sids[b1];
+                        myrow[cnt] = ((uint64_t)k0 << 32) | i0;
+                        if (two) myrow[cnt + 1] = ((uint64_t)k1 << 32) | i1;
+                        cnt += two ? 2 : 1;
+                    }
+                    __syncwarp();
+                }
+                c1 = clk();
+                pw[4] += c1 - c0;   // insertions
+                // make room: rows whose buffer cannot take another pass are compacted to the
+                // target rank (L, or the extrapolated rank for the fraction of columns seen)
+                uint32_t need = __ballot_sync(0xffffffffu, cnt > C - 32);
+                if (need) {
+                    uint32_t want = p.L, kmax = keep_max;
+                    if (p.alpha100) {
+                        const uint64_t seen = (uint64_t)ti * BN + (hp + 1) * 32;
+                        const uint64_t rr = (uint64_t)p.alpha100 * p.L * seen / (100ull * p.mb) + p.beta;
+                        if (rr < p.L) { want = (uint32_t)rr; kmax = want + (C - 32 - want) / 8; }
+                    }
+                    do {
+                        const int o = __ffs(need) - 1;
+                        need &= need - 1;
+                        const uint32_t c_o = __shfl_sync(0xffffffffu, cnt, o);
+                        uint64_t* ob = warprows + (uint64_t)o * C;
+                        uint32_t kept;
+                        uint32_t kth = select_keys<EPL>(ob, c_o, want, kmax, lane, &kept);
+                        // massive ties on the threshold key: split them by id (prefix of (key, id))
+                        if (kept > C - 32)
+                            kth = (uint32_t)(select_L<EPL>(ob, kept, want, kmax, hist, lane, &kept) >> 32);
+                        if (lane == (uint32_t)o) { cnt = kept; thr = ord2f(kth); }
+                    } while (need);
+                }
+                c0 = clk();
+                pw[2] += c0 - c1;   // compaction
+                };
+                // TMEM loads double-buffered: the next pass is loaded while this one is processed;
+                // the accumulator buffer is released once the last pass is in registers
+                uint32_t va[32], vb[32];
+                tmem_ld32_nowait(tb, va);
+#pragma unroll 1
+                for (uint32_t hp = 0; hp < BN / 32; hp += 2) {
                     tmem_wait_ld();
-                    if (hp == BN / 32 - 1) {
+                    tmem_ld32_nowait(tb + (hp + 1) * 32, vb);
+                    c0 = clk();
+                    pw[1] += c0 - c1;
+                    pass(va, hp);
+                    tmem_wait_ld();
+                    if (hp + 2 < BN / 32) {
+                        tmem_ld32_nowait(tb + (hp + 2) * 32, va);
+                    } else {
                         tc_fence_before();
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&bars->tm_empty[buf]);
                     }
-                    c0 = clk();
-                    pw[1] += c0 - c1;
-                    const uint32_t col0 = t * BN + hp * 32;
-                    if (p.noepi) {
-                        if ((v[0] ^ v[31]) == 0x7fc00001u) p.out_ids[0] = v[1];   // keep the loads live
-                        c1 = clk();
-                        continue;
-                    }
-                    if (p.probe) {
-                        if (valid) {
-#pragma unroll
-                            for (int j = 0; j < 32; j++)
-                                if (col0 + j < p.mb) p.probe[(uint64_t)row * p.mb + col0 + j] = __uint_as_float(v[j]);
-                        }
-                        c1 = clk();
-                        continue;
-                    }
-                    // reported id of this lane's column, fetched early (latency hidden by the mask)
-                    const uint32_t id0 = p.col_map ? __ldg(p.col_map + col0 + lane) : col0 + lane;
-                    c1 = clk();
-                    // strict test when columns arrive in increasing id, inclusive with the rotated sweep
-                    const float te = p.rotate ? next_up(thr) : thr;
-                    uint32_t mq[4] = {0, 0, 0, 0};
-#pragma unroll
-                    for (int s = 7; s >= 1; s -= 2) {
-#pragma unroll
-                        for (int g = 0; g < 4; g++) {
-                            const int j = g * 8 + s;
-                            uint32_t lo, hi;
-                            sub2(v[j - 1], v[j], te, lo, hi);
-                            mq[g] = __funnelshift_l(hi, mq[g], 1);
-                            mq[g] = __funnelshift_l(lo, mq[g], 1);
-                        }
-                    }
-                    uint32_t m = mq[0] | (mq[1] << 8) | (mq[2] << 16) | (mq[3] << 24);
-                    // self column: row r of block rb is column rb*RB + r
-                    if (scol - col0 < 32u) m &= ~(1u << (scol - col0));
-                    c0 = clk();
-                    pw[3] += c0 - c1;   // masks
-                    if (p.abl & 1) m = 0;
-                    if (__any_sync(0xffffffffu, m != 0)) {
-                        sids[lane] = id0;
-                        float4* st4 = (float4*)(skeys + lane * KSTRIDE);
-#pragma unroll
-                        for (int j4 = 0; j4 < 8; j4++)
-                            st4[j4] = make_float4(__uint_as_float(v[4 * j4]), __uint_as_float(v[4 * j4 + 1]),
-                                                  __uint_as_float(v[4 * j4 + 2]), __uint_as_float(v[4 * j4 + 3]));
-                        __syncwarp();
-                        if constexpr (PROF) pw[6] += __popc(m);
-                        // two candidates per iteration: independent smem loads and global stores
-                        const float* mykeys = skeys + lane * KSTRIDE;
-                        while (m) {
-                            if constexpr (PROF) pw[7]++;
-                            const uint32_t b0 = 31 - __clz(m);
-                            m ^= 1u << b0;
-                            const bool two = m != 0;
-                            const uint32_t b1 = two ? 31 - __clz(m) : b0;
-                            m &= ~(1u << b1);
-                            const uint32_t k0 = __float_as_uint(mykeys[b0]), i0 = sids[b0];
-                            const uint32_t k1 = __float_as_uint(mykeys[b1]), i1 = sids[b1];
-                            myrow[cnt] = ((uint64_t)k0 << 32) | i0;
-                            if (two) myrow[cnt + 1] = ((uint64_t)k1 << 32) | i1;
-                            cnt += two ? 2 : 1;
-                        }
-                        __syncwarp();
-                    }
-                    c1 = clk();
-                    pw[4] += c1 - c0;   // insertions
-                    // make room: rows whose buffer cannot take another pass are compacted to the
-                    // target rank (L, or the extrapolated rank for the fraction of columns seen)
-                    uint32_t need = __ballot_sync(0xffffffffu, cnt > C - 32);
-                    if (need) {
-                        uint32_t want = p.L, kmax = keep_max;
-                        if (p.alpha100) {
-                            const uint64_t seen = (uint64_t)ti * BN + (hp + 1) * 32;
-                            const uint64_t rr = (uint64_t)p.alpha100 * p.L * seen / (100ull * p.mb) + p.beta;
-                            if (rr < p.L) { want = (uint32_t)rr; kmax = want + (C - 32 - want) / 8; }
-                        }
-                        do {
-                            const int o = __ffs(need) - 1;
-                            need &= need - 1;
-                            const uint32_t c_o = __shfl_sync(0xffffffffu, cnt, o);
-                            uint64_t* ob = warprows + (uint64_t)o * C;
-                            uint32_t kept;
-                            uint32_t kth = select_keys<EPL>(ob, c_o, want, kmax, lane, &kept);
-                            // massive ties on the threshold key: split them by id (prefix of (key, id))
-                            if (kept > C - 32)
-                                kth = (uint32_t)(select_L<EPL>(ob, kept, want, kmax, hist, lane, &kept) >> 32);
-                            if (lane == (uint32_t)o) { cnt = kept; thr = ord2f(kth); }
-                        } while (need);
-                    }
-                    c0 = clk();
-                    pw[2] += c0 - c1;   // compaction
+                    pass(vb, hp + 1);
                 }
             }
             if (p.probe || p.noepi) continue;
