@@ -11,6 +11,11 @@
 //    placement would overflow a cluster; everything before it is exactly what the sequential
 //    pass does; the cluster closes (it never reopens) and speculation resumes at that vector.
 //    So a block costs <= k+1 rounds per phase and the result is bit-identical to the oracle.
+//    Default: assign_grid_kernel runs each round on the whole GPU (cooperative launch, grid
+//    barriers between count / cut / commit); assign_kernel (one CTA) stays as the reference
+//    variant (SG_PART_SINGLE_CTA=1).
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace sg {
@@ -252,6 +257,226 @@ __global__ void __launch_bounds__(K2_THREADS, 1) assign_kernel(PartArgs a) {
     if (tid == 0) a.state->status = st.status;
 }
 
+// ---------------------------------------------------------------------------------------------
+// K2 on the whole GPU: the same speculate-and-verify rounds, one round spread over G CTAs x GT
+// threads (a thread owns a contiguous segment of the block's vectors, CTAs in id order), with
+// grid-wide barriers between the steps of a round (count -> find the first overflow -> commit).
+// Cooperative launch guarantees the CTAs are co-resident.  Bit-identical to assign_kernel.
+constexpr int GT = 512;
+constexpr int MAXG = 1024;
+
+struct GridScratch {
+    unsigned bar_count, bar_gen;
+    unsigned long long cut;
+    unsigned cta_cnt[KMAX * MAXG];
+};
+
+__device__ __forceinline__ void grid_sync(GridScratch* g) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* gen = &g->bar_gen;
+        const unsigned my = *gen;
+        __threadfence();
+        if (atomicAdd(&g->bar_count, 1u) == gridDim.x - 1) {
+            g->bar_count = 0;
+            __threadfence();
+            atomicAdd(&g->bar_gen, 1u);
+        } else {
+            while (*gen == my) __nanosleep(64);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ uint32_t primary_choice(const PartArgs& a, uint64_t v, uint64_t open) {
+    const uint8_t* ov = a.order + v * a.k;
+    for (uint32_t i = 0; i < a.k; i++) if ((open >> ov[i]) & 1ull) return ov[i];
+    return 0;
+}
+
+// One speculate-and-verify round over [start, v1) of the current block.  PRIM: primaries, else
+// replicas.  Returns the cut (first vector not committed; ~0 when the whole range is done).
+template <bool PRIM>
+__device__ uint64_t grid_round(const PartArgs& a, PartState* gs, GridScratch* g, uint64_t start, uint64_t s0, uint64_t s1,
+                               uint64_t open, float tau, const float* radius, uint64_t* s_room,
+                               uint32_t (*s_wtot)[GT / 32], uint32_t* s_pre, unsigned long long* s_inc,
+                               unsigned long long* s_inc2, unsigned* s_rmax) {
+    const uint32_t k = a.k, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = GT / 32;
+    const uint64_t lo = max(start, s0);
+    uint32_t picks[KMAX];
+    auto count_mine = [&](uint32_t c) -> uint32_t {
+        uint32_t m = 0;
+        for (uint64_t v = lo; v < s1; v++) {
+            if (PRIM) {
+                m += primary_choice(a, v, open) == c;
+            } else {
+                const uint32_t np = replica_picks(a, v, open, tau, radius, picks);
+                for (uint32_t i = 0; i < np; i++) m += picks[i] == c;
+            }
+        }
+        return m;
+    };
+    // (a) per-cluster counts: warp-exclusive prefixes and per-warp totals, CTA totals to global
+    for (uint32_t c = 0; c < k; c++) {
+        const uint32_t mine = count_mine(c);
+        uint32_t inc = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= (uint32_t)o) inc += t;
+        }
+        if (lane == 31) s_wtot[c][warp] = inc;
+    }
+    __syncthreads();
+    if (tid < k) {
+        uint32_t run = 0;
+        for (uint32_t w = 0; w < nw; w++) { const uint32_t t = s_wtot[tid][w]; s_wtot[tid][w] = run; run += t; }
+        g->cta_cnt[tid * gridDim.x + blockIdx.x] = run;
+    }
+    grid_sync(g);
+    // (b) global prefix of this CTA; the thread whose segment holds the first overflow of c
+    //     proposes it as the cut
+    if (tid < k) {
+        uint32_t pre = 0;
+        for (uint32_t j = 0; j < blockIdx.x; j++) pre += ((volatile unsigned*)g->cta_cnt)[tid * gridDim.x + j];
+        s_pre[tid] = pre;
+    }
+    __syncthreads();
+    for (uint32_t c = 0; c < k; c++) {
+        const uint32_t mine = count_mine(c);
+        uint32_t inc = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= (uint32_t)o) inc += t;
+        }
+        const uint64_t pre = (uint64_t)s_pre[c] + s_wtot[c][warp] + inc - mine;
+        const uint64_t room = s_room[c];
+        if (pre <= room && pre + mine > room) {
+            const uint64_t need = room - pre + 1;
+            uint64_t seen = 0;
+            for (uint64_t v = lo; v < s1; v++) {
+                bool hit;
+                if (PRIM) {
+                    hit = primary_choice(a, v, open) == c;
+                } else {
+                    const uint32_t np = replica_picks(a, v, open, tau, radius, picks);
+                    hit = false;
+                    for (uint32_t i = 0; i < np; i++) hit |= picks[i] == c;
+                }
+                if (hit && ++seen == need) { atomicMin(&g->cut, (unsigned long long)v); break; }
+            }
+        }
+    }
+    grid_sync(g);
+    const uint64_t cut = *(volatile unsigned long long*)&g->cut;
+    // (c) commit [lo, cut) of my segment; state increments aggregated per CTA
+    if (tid < k) { s_inc[tid] = 0; s_inc2[tid] = 0; s_rmax[tid] = 0; }
+    __syncthreads();
+    for (uint64_t v = lo; v < min(s1, cut); v++) {
+        if (PRIM) {
+            const uint32_t c = primary_choice(a, v, open);
+            const float dv = a.dist[v * k + c];
+            a.home[v * a.omega] = c;
+            for (uint32_t h = 1; h < a.omega; h++) a.home[v * a.omega + h] = SG_SENT;
+            a.primary_d[v] = dv;
+            atomicAdd(&s_inc[c], 1ull);
+            atomicMax(&s_rmax[c], __float_as_uint(dv));   // d >= 0: int order == float order
+        } else {
+            const uint32_t np = replica_picks(a, v, open, tau, radius, picks);
+            for (uint32_t i = 0; i < np; i++) {
+                a.home[v * a.omega + 1 + i] = picks[i];
+                atomicAdd(&s_inc[picks[i]], 1ull);
+            }
+        }
+    }
+    __syncthreads();
+    if (tid < k && s_inc[tid]) {
+        atomicAdd((unsigned long long*)&gs->size[tid], s_inc[tid]);
+        if (PRIM) {
+            atomicAdd((unsigned long long*)&gs->prim[tid], s_inc[tid]);
+            atomicMax((unsigned*)&gs->radius[tid], s_rmax[tid]);
+        } else {
+            atomicAdd((unsigned long long*)&gs->repl[tid], s_inc[tid]);
+        }
+    }
+    (void)s_inc2;
+    grid_sync(g);
+    if (blockIdx.x == 0 && tid == 0) g->cut = ~0ull;   // read by everyone before the barrier above
+    return cut;
+}
+
+__global__ void __launch_bounds__(GT, 1) assign_grid_kernel(PartArgs a, PartState* gs, GridScratch* g) {
+    __shared__ uint64_t s_room[KMAX];
+    __shared__ uint32_t s_wtot[KMAX][GT / 32];
+    __shared__ uint32_t s_pre[KMAX];
+    __shared__ unsigned long long s_inc[KMAX], s_inc2[KMAX];
+    __shared__ unsigned s_rmax[KMAX];
+    __shared__ uint64_t s_open;
+    __shared__ float s_radius[KMAX];
+    const uint32_t k = a.k, tid = threadIdx.x;
+    const uint64_t T = (uint64_t)gridDim.x * GT, gtid = (uint64_t)blockIdx.x * GT + tid;
+    volatile PartState* vs = gs;
+    const uint64_t nblocks = (a.n + a.block - 1) / a.block;
+    for (uint64_t b = 0; b < nblocks; b++) {
+        const uint64_t v0 = b * a.block, v1 = min(a.n, v0 + a.block);
+        const uint64_t seg = (v1 - v0 + T - 1) / T;
+        const uint64_t s0 = min(v1, v0 + gtid * seg), s1 = min(v1, s0 + seg);
+        // ---------------- (1) primaries: nearest cluster with size < capacity
+        uint64_t start = v0;
+        while (true) {
+            if (tid == 0) {
+                uint64_t open = 0;
+                for (uint32_t c = 0; c < k; c++) if (vs->size[c] < a.cap) open |= 1ull << c;
+                s_open = open;
+            }
+            if (tid < k) s_room[tid] = a.cap - vs->size[tid];
+            __syncthreads();
+            const uint64_t open = s_open;
+            if (open == 0) { if (blockIdx.x == 0 && tid == 0) gs->status = SG_ERR_CAPACITY; break; }
+            const uint64_t cut = grid_round<true>(a, gs, g, start, s0, s1, open, 0.f, s_radius, s_room, s_wtot, s_pre,
+                                                  s_inc, s_inc2, s_rmax);
+            if (cut == ~0ull) break;
+            start = cut;
+        }
+        if (s_open == 0) break;
+        // ---------------- (2) statistics and thresholds (R4, R5)
+        const float tau = __fadd_rn(1.0f, __fdiv_rn(a.alpha, (float)(1 + b)));
+        if (blockIdx.x == 0 && tid == 0) {
+            uint64_t P = 0;
+            for (uint32_t c = 0; c < k; c++) P += vs->prim[c];
+            for (uint32_t c = 0; c < k; c++) gs->budget[c] = budget_of(vs->prim[c], P, k, a.theta0, a.cap);
+        }
+        grid_sync(g);
+        // ---------------- (3) Algorithm 1 replicas, speculate-and-verify
+        if (a.omega > 1) {
+            start = v0;
+            while (true) {
+                if (tid == 0) {
+                    uint64_t open = 0;
+                    for (uint32_t c = 0; c < k; c++)
+                        if (vs->size[c] < a.cap && vs->repl[c] < vs->budget[c]) open |= 1ull << c;
+                    s_open = open;
+                }
+                if (tid < k) {
+                    const uint64_t r1 = a.cap - vs->size[tid], r2 = vs->budget[tid] - vs->repl[tid];
+                    s_room[tid] = r1 < r2 ? r1 : r2;
+                    s_radius[tid] = vs->radius[tid];   // updated by other CTAs' atomics: no L1 copy
+                }
+                __syncthreads();
+                const uint64_t open = s_open;
+                if (open == 0) break;
+                const uint64_t cut = grid_round<false>(a, gs, g, start, s0, s1, open, tau, s_radius, s_room, s_wtot,
+                                                       s_pre, s_inc, s_inc2, s_rmax);
+                if (cut == ~0ull) break;
+                start = cut;
+            }
+        }
+        __syncthreads();
+    }
+}
+
 }  // namespace
 
 uint64_t derive_capacity(uint64_t n, uint32_t k, uint32_t t) {
@@ -266,6 +491,7 @@ size_t partition_ws(uint64_t n, uint32_t k) {
     cv.take<float>(n * k);
     cv.take<uint8_t>(n * k);
     cv.take<PartState>(1);
+    cv.take<GridScratch>(1);
     return cv.off + 1024;
 }
 
@@ -276,6 +502,7 @@ sg_status partition_run(const void* x, sg_dtype dtype, uint64_t n, uint32_t d, c
     float* dist = cv.take<float>(n * p->k);
     uint8_t* order = cv.take<uint8_t>(n * p->k);
     PartState* state = cv.take<PartState>(1);
+    GridScratch* gscr = cv.take<GridScratch>(1);
     if (!cv.ok()) { set_error("partition: workspace too small"); return SG_ERR_WORKSPACE; }
     const uint64_t cap = p->capacity ? p->capacity : derive_capacity(n, p->k, p->theta0_ppm);
     SG_CHECK_ARG(cap * p->k >= n, "partition: capacity * k < n");
@@ -286,10 +513,29 @@ sg_status partition_run(const void* x, sg_dtype dtype, uint64_t n, uint32_t d, c
     a.dist = dist; a.order = order; a.home = home; a.primary_d = primary_d; a.state = state;
     a.n = n; a.cap = cap; a.k = p->k; a.omega = p->omega; a.block = p->block_size; a.theta0 = p->theta0_ppm;
     a.eps = p->epsilon; a.alpha = p->alpha;
-    const size_t smem = (size_t)p->k * K2_THREADS * sizeof(uint16_t);
-    SG_CUDA(cudaFuncSetAttribute(assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    assign_kernel<<<1, K2_THREADS, smem, st>>>(a);
-    SG_LAUNCHED("assign_kernel");
+    static int single = -1;
+    if (single < 0) { const char* e = getenv("SG_PART_SINGLE_CTA"); single = e ? atoi(e) : 0; }
+    if (single) {   // one-CTA reference variant of K2 (kept for comparison)
+        const size_t smem = (size_t)p->k * K2_THREADS * sizeof(uint16_t);
+        SG_CUDA(cudaFuncSetAttribute(assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        assign_kernel<<<1, K2_THREADS, smem, st>>>(a);
+        SG_LAUNCHED("assign_kernel");
+    } else {
+        SG_CUDA(cudaMemsetAsync(state, 0, sizeof(PartState), st));
+        SG_CUDA(cudaMemsetAsync(gscr, 0, sizeof(GridScratch), st));
+        SG_CUDA(cudaMemsetAsync(&gscr->cut, 0xFF, sizeof(unsigned long long), st));
+        int per_sm = 0;
+        SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, assign_grid_kernel, GT, 0));
+        const uint64_t need = (p->block_size + GT - 1) / GT;   // at most one vector per thread per block
+        uint64_t g = (uint64_t)num_sms() * (per_sm > 0 ? 1 : 0);
+        if (g > need) g = need;
+        if (g > MAXG) g = MAXG;
+        if (g < 1) g = 1;
+        PartState* gs = state;
+        void* args[] = {(void*)&a, (void*)&gs, (void*)&gscr};
+        SG_CUDA(cudaLaunchCooperativeKernel((const void*)assign_grid_kernel, dim3((unsigned)g), dim3(GT), args, 0, st));
+        SG_LAUNCHED("assign_grid_kernel");
+    }
     PartState hs;
     SG_CUDA(cudaMemcpyAsync(&hs, state, sizeof(PartState), cudaMemcpyDeviceToHost, st));
     SG_CUDA(cudaStreamSynchronize(st));
