@@ -29,8 +29,11 @@ namespace sg {
 namespace {
 
 // ----------------------------------------------------------------- the kernel
+constexpr uint32_t NEPI_R = 16;                         // epilogue warps (2 column streams x 8)
+constexpr uint32_t NTHREADS_R = 64 + NEPI_R * 32;
+
 template <int KIND, int NKA, int MINI, int EPL>
-__global__ void __launch_bounds__(NTHREADS, 1)
+__global__ void __launch_bounds__(NTHREADS_R, 1)
 knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmAm, const __grid_constant__ CUtensorMap tmBm, KnnParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -50,7 +53,9 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     uint8_t* sB = smem + NACC * AHALF;
     Bars* bars = (Bars*)(sB + p.stages * SLOT);
     uint8_t* bars_end = (uint8_t*)(bars + 1);
-    uint8_t* scratch_all = bars_end + ((128u - (smem_u32(bars_end) & 127u)) & 127u);   // NEPI x SCRATCH
+    unsigned long long* s_pair = (unsigned long long*)(bars_end + ((128u - (smem_u32(bars_end) & 127u)) & 127u));
+    uint32_t (*s_cnt)[BM] = (uint32_t (*)[BM])(s_pair + BM);          // [2][BM] stream counts
+    uint8_t* scratch_all = (uint8_t*)(s_pair + BM) + 2 * BM * 4;       // NEPI_R x SCRATCH
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // fallback launch: the number of A rows is known only on the device
@@ -177,43 +182,42 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             }
         }
     } else {
-        // ===================== epilogue: fused selection =====================
-        const uint32_t e = warp - 2, q = warp & 3, a = e >> 2;
+        // ===================== epilogue: fused selection, two column streams =====================
+        // Warps 2..17.  Stream s takes the tiles of parity s (= its TMEM buffers), q = warp % 4 is
+        // the TMEM lane quadrant, a the row half; thread = one row.  Each (row, stream) has its
+        // own candidate buffer; the row threshold is ONE (key, id) pair in shared memory shared by
+        // the two streams and lowered with atomicMin when either compacts.  The insertion test is
+        // inclusive (key <= thr: equal keys with a larger id may enter, above the pair), so each
+        // buffer holds every column of its stream at or below the final pair T, for any order; a
+        // row is exact iff >= L union entries lie at or below T (always so with rank-L thresholds;
+        // with extrapolated ones a row that misses it goes to the fallback launch).
+        const uint32_t e = warp - 2, s = e >> 3, q = warp & 3, a = (e & 7) >> 2;
         const uint32_t r = a * MSUB + q * 32 + lane;         // row within the block
-        uint8_t* scratch = scratch_all + e * SCRATCH;
+        uint8_t* scratch = scratch_all + (s * 4 * NACC + (e & 7)) * SCRATCH;   // active warps only
         float* skeys = (float*)scratch;                      // [32][KSTRIDE] staged keys
         uint32_t* hist = (uint32_t*)scratch;                 // 256 (aliases skeys)
         uint64_t* sortbuf = (uint64_t*)scratch;              // 512 (aliases skeys)
         uint32_t* sids = (uint32_t*)(scratch + 32 * KSTRIDE * 4);   // 64 reported ids of the tile
         const uint32_t C = p.C;
         const uint32_t keep_max = p.keep_max;                // in-loop compaction target (>= L)
-        uint64_t* myrow = p.cand + ((uint64_t)blockIdx.x * BM + r) * C;
-        uint64_t* warprows = p.cand + ((uint64_t)blockIdx.x * BM + a * MSUB + q * 32) * C;
-        const float INF = __int_as_float(0x7f800000);
+        auto rowbuf = [&](uint32_t R, uint32_t st) -> uint64_t* {
+            return p.cand + (((uint64_t)blockIdx.x * 2 + st) * BM + R) * C;
+        };
+        uint64_t* myrow = rowbuf(r, s);
+        uint64_t* warprows = rowbuf(a * MSUB + q * 32, s);
         const uint32_t tl = tmem + ((q * 32) << 16) + a * NBUF * BN;
+        const uint64_t PINIT = pair_ord(3.40282347e38f, SG_SENT);   // every finite key passes, +inf not
+        const uint32_t nbar = NACC * 8 * 32;                 // active epilogue threads
         uint32_t git = 0;
         for (uint32_t rb = blockIdx.x; rb < n_rb && a < NACC; rb += gridDim.x) {
             const uint32_t row = rb * RB + r;
             const bool valid = row < ma;
             const uint32_t scol = p.self_exclude ? (p.self_col ? (valid ? p.self_col[row] : SG_SENT) : row) : SG_SENT;
-            float thr = valid ? INF : -INF;
             uint32_t cnt = 0;
-            if constexpr (ATM) {
-                // this row's A operand into TMEM (lane = row, K packed 2 per column); all MMAs of
-                // the previous row block completed before its last tile reached this warp
-                const uint4* src = p.a_glob + (uint64_t)row * (p.a_words / 4);
-                const uint32_t ta = tmem + ((q * 32) << 16) + ACOL + a * 128;
-                for (uint32_t c = 0; c < p.a_words; c += 8) {
-                    const uint4 u0 = __ldg(src + c / 4), u1 = __ldg(src + c / 4 + 1);
-                    const uint32_t w8[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
-                    tmem_st8(ta + c, w8);
-                }
-                tmem_wait_st();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&bars->a_full);
-            }
+            if (s == 0) s_pair[r] = valid ? PINIT : pair_ord(-__int_as_float(0x7f800000), 0);
+            named_bar_sync(1, nbar);
             for (uint32_t ti = 0, t = tile_at(p, rb, 0); ti < p.n_ct; ti++, git++, t = t + 1 == p.n_ct ? 0 : t + 1) {
+                if ((git & 1u) != s) continue;               // the other stream's tile
                 const uint32_t buf = git % NBUF;
                 long long c0 = clk();
                 mbar_wait(&bars->tm_full[buf], (git / NBUF) & 1);
@@ -221,152 +225,152 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 pw[0] += c1 - c0;
                 tc_fence_after();
                 const uint32_t tb = tl + buf * BN;
-                // one 32-column pass (register budget: 10 warps x 168 registers)
-                auto pass = [&](uint32_t (&v)[32], const uint32_t hp) {
-                const uint32_t col0 = t * BN + hp * 32;
-                if (p.noepi) {
-                    if ((v[0] ^ v[31]) == 0x7fc00001u) p.out_ids[0] = v[1];   // keep the loads live
-                    c1 = clk();
-                    return;
-                }
-                if (p.probe) {
-                    if (valid) {
-#pragma unroll
-                        for (int j = 0; j < 32; j++)
-                            if (col0 + j < p.mb) p.probe[(uint64_t)row * p.mb + col0 + j] = __uint_as_float(v[j]);
-                    }
-                    c1 = clk();
-                    return;
-                }
-                // reported id of this lane's column, fetched early (latency hidden by the mask)
-                const uint32_t id0 = p.col_map ? __ldg(p.col_map + col0 + lane) : col0 + lane;
-                c1 = clk();
-                // strict test when columns arrive in increasing id, inclusive with the rotated sweep
-                const float te = p.rotate ? next_up(thr) : thr;
-                uint32_t mq[4] = {0, 0, 0, 0};
-#pragma unroll
-                for (int s = 7; s >= 1; s -= 2) {
-#pragma unroll
-                    for (int g = 0; g < 4; g++) {
-                        const int j = g * 8 + s;
-                        uint32_t lo, hi;
-                        sub2(v[j - 1], v[j], te, lo, hi);
-                        mq[g] = __funnelshift_l(hi, mq[g], 1);
-                        mq[g] = __funnelshift_l(lo, mq[g], 1);
-                    }
-                }
-                uint32_t m = mq[0] | (mq[1] << 8) | (mq[2] << 16) | (mq[3] << 24);
-                // self column: row r of block rb is column rb*RB + r
-                if (scol - col0 < 32u) m &= ~(1u << (scol - col0));
-                c0 = clk();
-                pw[3] += c0 - c1;   // masks
-                if (p.abl & 1) m = 0;
-                if (__any_sync(0xffffffffu, m != 0)) {
-                    sids[lane] = id0;
-                    float4* st4 = (float4*)(skeys + lane * KSTRIDE);
-#pragma unroll
-                    for (int j4 = 0; j4 < 8; j4++)
-                        st4[j4] = make_float4(__uint_as_float(v[4 * j4]), __uint_as_float(v[4 * j4 + 1]),
-                                              __uint_as_float(v[4 * j4 + 2]), __uint_as_float(v[4 * j4 + 3]));
-                    __syncwarp();
-                    if constexpr (PROF) pw[6] += __popc(m);
-                    // two candidates per iteration: independent smem loads and global stores
-                    const float* mykeys = skeys + lane * KSTRIDE;
-                    while (m) {
-                        if constexpr (PROF) pw[7]++;
-                        const uint32_t b0 = 31 - __clz(m);
-                        m ^= 1u << b0;
-                        const bool two = m != 0;
-                        const uint32_t b1 = two ? 31 - __clz(m) : b0;
-                        m &= ~(1u << b1);
-                        const uint32_t k0 = __float_as_uint(mykeys[b0]), i0 = sids[b0];
-                        const uint32_t k1 = __float_as_uint(mykeys[b1]), i1 = sids[b1];
-                        myrow[cnt] = ((uint64_t)k0 << 32) | i0;
-                        if (two) myrow[cnt + 1] = ((uint64_t)k1 << 32) | i1;
-                        cnt += two ? 2 : 1;
-                    }
-                    __syncwarp();
-                }
-                c1 = clk();
-                pw[4] += c1 - c0;   // insertions
-                // make room: rows whose buffer cannot take another pass are compacted to the
-                // target rank (L, or the extrapolated rank for the fraction of columns seen)
-                uint32_t need = __ballot_sync(0xffffffffu, cnt > C - 32);
-                if (need) {
-                    uint32_t want = p.L, kmax = keep_max;
-                    if (p.alpha100) {
-                        const uint64_t seen = (uint64_t)ti * BN + (hp + 1) * 32;
-                        const uint64_t rr = (uint64_t)p.alpha100 * p.L * seen / (100ull * p.mb) + p.beta;
-                        if (rr < p.L) { want = (uint32_t)rr; kmax = want + (C - 32 - want) / 8; }
-                    }
-                    do {
-                        const int o = __ffs(need) - 1;
-                        need &= need - 1;
-                        const uint32_t c_o = __shfl_sync(0xffffffffu, cnt, o);
-                        uint64_t* ob = warprows + (uint64_t)o * C;
-                        uint32_t kept;
-                        uint32_t kth = select_keys<EPL>(ob, c_o, want, kmax, lane, &kept);
-                        // massive ties on the threshold key: split them by id (prefix of (key, id))
-                        if (kept > C - 32)
-                            kth = (uint32_t)(select_L<EPL>(ob, kept, want, kmax, hist, lane, &kept) >> 32);
-                        if (lane == (uint32_t)o) { cnt = kept; thr = ord2f(kth); }
-                    } while (need);
-                }
-                c0 = clk();
-                pw[2] += c0 - c1;   // compaction
-                };
-                // TMEM loads double-buffered: the next pass is loaded while this one is processed;
-                // the accumulator buffer is released once the last pass is in registers
-                uint32_t va[32], vb[32];
-                tmem_ld32_nowait(tb, va);
+                // the row threshold (possibly lowered by the other stream) for this tile
+                const float te = next_up(ord2f((uint32_t)(*(volatile unsigned long long*)&s_pair[r] >> 32)));
 #pragma unroll 1
-                for (uint32_t hp = 0; hp < BN / 32; hp += 2) {
+                for (uint32_t hp = 0; hp < BN / 32; hp++) {
+                    uint32_t v[32];
+                    tmem_ld32_nowait(tb + hp * 32, v);
                     tmem_wait_ld();
-                    tmem_ld32_nowait(tb + (hp + 1) * 32, vb);
-                    c0 = clk();
-                    pw[1] += c0 - c1;
-                    pass(va, hp);
-                    tmem_wait_ld();
-                    if (hp + 2 < BN / 32) {
-                        tmem_ld32_nowait(tb + (hp + 2) * 32, va);
-                    } else {
+                    if (hp == BN / 32 - 1) {
                         tc_fence_before();
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&bars->tm_empty[buf]);
                     }
-                    pass(vb, hp + 1);
+                    c0 = clk();
+                    pw[1] += c0 - c1;
+                    const uint32_t col0 = t * BN + hp * 32;
+                    if (p.noepi) {
+                        if ((v[0] ^ v[31]) == 0x7fc00001u) p.out_ids[0] = v[1];   // keep the loads live
+                        continue;
+                    }
+                    if (p.probe) {
+                        if (valid) {
+#pragma unroll
+                            for (int j = 0; j < 32; j++)
+                                if (col0 + j < p.mb) p.probe[(uint64_t)row * p.mb + col0 + j] = __uint_as_float(v[j]);
+                        }
+                        continue;
+                    }
+                    const uint32_t id0 = p.col_map ? __ldg(p.col_map + col0 + lane) : col0 + lane;
+                    // pass mask: bit j set iff key(j) < te, i.e. key(j) <= thr
+                    uint32_t mq[4] = {0, 0, 0, 0};
+#pragma unroll
+                    for (int s2 = 7; s2 >= 1; s2 -= 2) {
+#pragma unroll
+                        for (int g = 0; g < 4; g++) {
+                            const int j = g * 8 + s2;
+                            uint32_t lo, hi;
+                            sub2(v[j - 1], v[j], te, lo, hi);
+                            mq[g] = __funnelshift_l(hi, mq[g], 1);
+                            mq[g] = __funnelshift_l(lo, mq[g], 1);
+                        }
+                    }
+                    uint32_t m = mq[0] | (mq[1] << 8) | (mq[2] << 16) | (mq[3] << 24);
+                    if (scol - col0 < 32u) m &= ~(1u << (scol - col0));   // self column
+                    c1 = clk();
+                    pw[3] += c1 - c0;
+                    if (p.abl & 1) m = 0;
+                    if (__any_sync(0xffffffffu, m != 0)) {
+                        sids[lane] = id0;
+                        float4* st4 = (float4*)(skeys + lane * KSTRIDE);
+#pragma unroll
+                        for (int j4 = 0; j4 < 8; j4++)
+                            st4[j4] = make_float4(__uint_as_float(v[4 * j4]), __uint_as_float(v[4 * j4 + 1]),
+                                                  __uint_as_float(v[4 * j4 + 2]), __uint_as_float(v[4 * j4 + 3]));
+                        __syncwarp();
+                        if constexpr (PROF) pw[6] += __popc(m);
+                        const float* mykeys = skeys + lane * KSTRIDE;
+                        while (m) {   // two candidates per iteration
+                            if constexpr (PROF) pw[7]++;
+                            const uint32_t b0 = 31 - __clz(m);
+                            m ^= 1u << b0;
+                            const bool two = m != 0;
+                            const uint32_t b1 = two ? 31 - __clz(m) : b0;
+                            m &= ~(1u << b1);
+                            const uint32_t k0 = __float_as_uint(mykeys[b0]), i0 = sids[b0];
+                            const uint32_t k1 = __float_as_uint(mykeys[b1]), i1 = sids[b1];
+                            myrow[cnt] = ((uint64_t)k0 << 32) | i0;
+                            if (two) myrow[cnt + 1] = ((uint64_t)k1 << 32) | i1;
+                            cnt += two ? 2 : 1;
+                        }
+                        __syncwarp();
+                    }
+                    c0 = clk();
+                    pw[4] += c0 - c1;
+                    // make room: compact rows whose buffer cannot take another pass to the target
+                    // rank per stream (L, or the extrapolated rank for the fraction seen) under the
+                    // row threshold, and lower the shared pair
+                    uint32_t need = __ballot_sync(0xffffffffu, cnt > C - 32);
+                    if (need) {
+                        uint32_t want = p.L, kmax = keep_max;
+                        if (p.alpha100) {
+                            const uint64_t seen = (uint64_t)ti * BN + (hp + 1) * 32;
+                            const uint64_t rr = (uint64_t)p.alpha100 * p.L * seen / (200ull * p.mb) + p.beta;
+                            if (rr < p.L) { want = (uint32_t)rr; kmax = want + (C - 32 - want) / 8; }
+                        }
+                        do {
+                            const int o = __ffs(need) - 1;
+                            need &= need - 1;
+                            const uint32_t c_o = __shfl_sync(0xffffffffu, cnt, o);
+                            const uint32_t R = a * MSUB + q * 32 + o;
+                            uint64_t* ob = warprows + (uint64_t)o * C;
+                            const uint64_t cap = *(volatile unsigned long long*)&s_pair[R];
+                            uint32_t kept;
+                            uint64_t P = select_pairs<EPL>(ob, c_o, cap, want, kmax, lane, &kept);
+                            if (kept > C - 32)   // massive ties on the threshold key: split them by id
+                                P = select_L<EPL>(ob, kept, want, kmax, hist, lane, &kept);
+                            if (lane == (uint32_t)o) {
+                                cnt = kept;
+                                atomicMin(&s_pair[R], (unsigned long long)P);
+                            }
+                        } while (need);
+                    }
+                    c1 = clk();
+                    pw[2] += c1 - c0;
                 }
             }
             if (p.probe || p.noepi) continue;
             const long long f0 = clk();
-            // ---- final: exact top-L of each of the warp's rows, sorted by (dist, id)
-            __syncwarp();
-            for (uint32_t o = 0; o < 32; o++) {
-                uint32_t c_o = __shfl_sync(0xffffffffu, cnt, o);
-                const uint32_t row_o = rb * RB + a * MSUB + q * 32 + o;
+            s_cnt[s][r] = cnt;
+            named_bar_sync(1, nbar);
+            // ---- final: union of the row's two stream buffers, exactness check, sorted top-L;
+            //      the 32 rows of this (q, a) group are split between its two stream warps
+            for (uint32_t o = 16 * s; o < 16 * s + 16; o++) {
+                const uint32_t R = a * MSUB + q * 32 + o;
+                const uint32_t row_o = rb * RB + R;
                 if (row_o >= ma) continue;
-                if (p.alpha100 && c_o < p.L) {
+                const uint64_t P = s_pair[R];
+                uint64_t* bb[2] = {rowbuf(R, 0), rowbuf(R, 1)};
+                uint32_t cc[2] = {s_cnt[0][R], s_cnt[1][R]};
+                uint32_t n_le = 0;
+#pragma unroll
+                for (int st = 0; st < 2; st++) {
+                    uint32_t kept;
+                    if (cc[st] > p.L) {   // a stream's own top-L holds all its entries of the row's top-L
+                        select_pairs<EPL>(bb[st], cc[st], P, p.L, p.L, lane, &kept);
+                        if (kept > SORT_MAX / 2) {
+                            select_L<EPL>(bb[st], kept, p.L, p.L, hist, lane, &kept);
+                            kept = p.L;
+                        }
+                        cc[st] = kept;
+                    }
+                    for (uint32_t i0 = 0; i0 < cc[st]; i0 += 32) {
+                        const uint32_t i = i0 + lane;
+                        n_le += __popc(__ballot_sync(0xffffffffu, i < cc[st] && raw2ord(bb[st][i]) <= P));
+                    }
+                }
+                if (p.alpha100 && P != PINIT && n_le < p.L) {
                     // extrapolated threshold was too tight for this row: recompute it (fallback)
                     if (lane == 0) p.fail_rows[atomicAdd(p.fail_count, 1u)] = row_o;
                     continue;
                 }
-                uint64_t* b0 = warprows + (uint64_t)o * C;
-                if (c_o > p.L) {
-                    // every key <= the L-th smallest key (finish_row sorts them and writes L);
-                    // exact (key, id) selection only if ties would overflow the sort buffer
-                    uint32_t kept;
-                    select_keys<EPL>(b0, c_o, p.L, p.L, lane, &kept);
-                    if (kept > SORT_MAX) {
-                        select_L<EPL>(b0, kept, p.L, p.L, hist, lane, &kept);
-                        kept = p.L;
-                    }
-                    c_o = kept;
-                }
                 const uint64_t orow = p.row_map ? p.row_map[row_o] : row_o;
-                finish_row(b0, c_o, b0, 0, p.L, sortbuf, p.norm_a[row_o], p.out_ids + orow * p.L,
+                finish_row(bb[0], cc[0], bb[1], cc[1], p.L, sortbuf, p.norm_a[row_o], p.out_ids + orow * p.L,
                            p.out_d + orow * p.L, lane);
             }
-            pw[5] += clk() - f0;   // final phase
+            named_bar_sync(1, nbar);   // buffers and thresholds are reused by the next row block
+            pw[5] += clk() - f0;
         }
     }
     if (PROF && p.prof && lane == 0)
@@ -400,7 +404,7 @@ template <int KIND, int NKA, int MINI, int EPL>
 sg_status launch_t(const CUtensorMap* maps, KnnParams& p, cudaStream_t st) {
     constexpr uint32_t AHALF = (KIND == 0 && SG_ATM) ? 0u : NKA * ATOM + (MINI ? MINIB : 0u);   // A in TMEM for f16
     constexpr uint32_t NACC = KIND == 0 ? NACC_MAX : 1;
-    const size_t fixed = NACC * AHALF + sizeof(Bars) + 128 + NEPI * SCRATCH + 1024 + 64;
+    const size_t fixed = NACC * AHALF + sizeof(Bars) + 128 + BM * 8 + 2 * BM * 4 + 8 * NACC * SCRATCH + 1024 + 64;
     const size_t budget = 227 * 1024;
     if (fixed + (NKA + MINI) * SLOT > budget) { set_error("kNN: operand too wide for shared memory"); return SG_ERR_UNSUPPORTED; }
     uint32_t stages = (uint32_t)((budget - fixed) / SLOT);
@@ -411,7 +415,7 @@ sg_status launch_t(const CUtensorMap* maps, KnnParams& p, cudaStream_t st) {
     SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const uint32_t grid = p.n_rb < (uint32_t)num_sms() ? p.n_rb : (uint32_t)num_sms();
     knn_time_begin(st);
-    kern<<<grid, NTHREADS, smem, st>>>(maps[0], maps[1], maps[2], maps[3], p);
+    kern<<<grid, NTHREADS_R, smem, st>>>(maps[0], maps[1], maps[2], maps[3], p);
     SG_LAUNCHED("knn_tc_kernel");
     knn_time_end(st);
     return SG_OK;
@@ -450,7 +454,7 @@ static bool use_transposed(uint32_t L) {
     return on && L <= 128;
 }
 static size_t cand_words_per_cta(uint32_t L) {
-    const size_t row_major = (size_t)BM * cand_cap(L);
+    const size_t row_major = 2 * (size_t)BM * cand_cap(L);   // two column streams
     const size_t transposed = use_transposed(L) ? (size_t)BM * 4 * knn_t_cap(L, false) : 0;
     return row_major > transposed ? row_major : transposed;
 }

@@ -52,76 +52,6 @@ __host__ __device__ constexpr uint32_t instr_desc_t(uint32_t n) {
     return (1u << 4) | ((KIND ? 2u : 0u) << 7) | ((KIND ? 2u : 0u) << 10) | ((n >> 3) << 17) | ((MSUB >> 4) << 24);
 }
 
-__device__ __forceinline__ uint64_t pair_ord(float key, uint32_t id) { return ((uint64_t)f2ord(key) << 32) | id; }
-
-// Compaction of one stream buffer rb[0..cnt) (raw words) under the row threshold pair `cap`:
-// entries above `cap` are dropped; of the rest, if more than keep_max remain, only those with key
-// <= T are kept, T found by bit descent on the ordered key (count(key <= T) >= want, stopping as
-// soon as it is <= keep_max, else the smallest such T; ties on T are never split).  Returns the
-// new threshold pair (T, SENT), or `cap` when nothing had to be selected.  All lanes call.
-template <int EPL>
-__device__ __forceinline__ uint64_t select_pairs(uint64_t* rb, uint32_t cnt, uint64_t cap, uint32_t want,
-                                                 uint32_t keep_max, uint32_t lane, uint32_t* kept) {
-    uint64_t e[EPL];
-    uint32_t k[EPL];
-    uint32_t n = 0;
-#pragma unroll
-    for (int i = 0; i < EPL; i++) {
-        const uint32_t idx = i * 32 + lane;
-        e[i] = idx < cnt ? rb[idx] : 0ull;
-        const uint64_t po = raw2ord(e[i]);
-        const bool in = idx < cnt && po <= cap;
-        k[i] = in ? (uint32_t)(po >> 32) : 0xFFFFFFFFu;
-        n += __popc(__ballot_sync(0xffffffffu, in));
-    }
-    uint64_t P = cap;
-    uint32_t T = 0xFFFFFFFEu;                   // keep every entry at or below cap
-    if (n > keep_max && n > want) {
-        uint32_t lo = 0xFFFFFFFFu, hi = 0;
-#pragma unroll
-        for (int i = 0; i < EPL; i++)
-            if (k[i] != 0xFFFFFFFFu) { lo = min(lo, k[i]); hi = max(hi, k[i]); }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-            hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-        }
-        T = hi;
-        if (lo != hi) {
-            int b = 31 - __clz(lo ^ hi);
-            uint32_t pfx = b >= 31 ? 0u : lo & ~((2u << b) - 1u);
-            bool done = false;
-#pragma unroll 1
-            for (; b >= 0; b--) {
-                const uint32_t t = pfx | ((1u << b) - 1u);
-                uint32_t c = 0;
-#pragma unroll
-                for (int i = 0; i < EPL; i++) c += __popc(__ballot_sync(0xffffffffu, k[i] <= t));
-                if (c >= want) {
-                    T = t;
-                    if (c <= keep_max) { done = true; break; }
-                } else {
-                    pfx |= 1u << b;
-                }
-            }
-            if (!done) T = pfx;
-        }
-        const uint64_t PT = ((uint64_t)T << 32) | SG_SENT;
-        P = PT < cap ? PT : cap;
-    }
-    uint32_t base = 0;
-#pragma unroll
-    for (int i = 0; i < EPL; i++) {
-        const bool sel = k[i] <= T;
-        const uint32_t bal = __ballot_sync(0xffffffffu, sel);
-        if (sel) rb[base + __popc(bal & ((1u << lane) - 1u))] = e[i];
-        base += __popc(bal);
-    }
-    __syncwarp();
-    *kept = base;
-    return P;
-}
-
 template <int KIND, int NKA, int MINI, int CS>
 __global__ void __launch_bounds__(NTHREADS, 1)
 knn_tct_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
