@@ -69,7 +69,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         for (uint32_t s = 0; s < p.stages; s++) { mbar_init(&bars->full[s], 1); mbar_init(&bars->empty[s], 1); }
         mbar_init(&bars->a_full, ATM ? 4 * NACC : 1);
         mbar_init(&bars->a_empty, 1);
-        for (uint32_t b = 0; b < NBUF_MAX; b++) { mbar_init(&bars->tm_full[b], 1); mbar_init(&bars->tm_empty[b], 4 * NACC); }
+        for (uint32_t b = 0; b < NBUF_MAX; b++) { mbar_init(&bars->tm_full[b], 1); mbar_init(&bars->tm_empty[b], 8 * NACC); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -183,8 +183,9 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         }
     } else {
         // ===================== epilogue: fused selection, two column streams =====================
-        // Warps 2..17.  Stream s takes the tiles of parity s (= its TMEM buffers), q = warp % 4 is
-        // the TMEM lane quadrant, a the row half; thread = one row.  Each (row, stream) has its
+        // Warps 2..17.  Stream s takes columns [64 s, 64 s + 64) of every tile (both streams drain
+        // the same TMEM buffer while the MMA fills the other), q = warp % 4 is the TMEM lane
+        // quadrant, a the row half; thread = one row.  Each (row, stream) has its
         // own candidate buffer; the row threshold is ONE (key, id) pair in shared memory shared by
         // the two streams and lowered with atomicMin when either compacts.  The insertion test is
         // inclusive (key <= thr: equal keys with a larger id may enter, above the pair), so each
@@ -217,7 +218,6 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             if (s == 0) s_pair[r] = valid ? PINIT : pair_ord(-__int_as_float(0x7f800000), 0);
             named_bar_sync(1, nbar);
             for (uint32_t ti = 0, t = tile_at(p, rb, 0); ti < p.n_ct; ti++, git++, t = t + 1 == p.n_ct ? 0 : t + 1) {
-                if ((git & 1u) != s) continue;               // the other stream's tile
                 const uint32_t buf = git % NBUF;
                 long long c0 = clk();
                 mbar_wait(&bars->tm_full[buf], (git / NBUF) & 1);
@@ -228,11 +228,11 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 // the row threshold (possibly lowered by the other stream) for this tile
                 const float te = next_up(ord2f((uint32_t)(*(volatile unsigned long long*)&s_pair[r] >> 32)));
 #pragma unroll 1
-                for (uint32_t hp = 0; hp < BN / 32; hp++) {
+                for (uint32_t hp = s * (BN / 64); hp < (s + 1) * (BN / 64); hp++) {   // this stream's passes
                     uint32_t v[32];
                     tmem_ld32_nowait(tb + hp * 32, v);
                     tmem_wait_ld();
-                    if (hp == BN / 32 - 1) {
+                    if (hp == (s + 1) * (BN / 64) - 1) {
                         tc_fence_before();
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&bars->tm_empty[buf]);
