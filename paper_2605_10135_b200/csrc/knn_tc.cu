@@ -564,7 +564,7 @@ sg_status knn_core(const Operand& A, const Operand& B, int /*metric*/, bool self
     if (!cv.ok()) { set_error("kNN: workspace too small (fallback)"); return SG_ERR_WORKSPACE; }
     SG_CUDA(cudaMemsetAsync(fail_count, 0, sizeof(uint32_t), st));
     p.alpha100 = (uint32_t)alpha;
-    p.beta = (uint32_t)(beta >= 0 ? beta : tr ? 6 : 8);   // per stream (transposed) / per row
+    p.beta = (uint32_t)(beta >= 0 ? beta : tr ? 6 : 12);   // per column stream
     p.eager = (uint32_t)eager;
     p.fail_count = fail_count;
     p.fail_rows = fail_rows;
