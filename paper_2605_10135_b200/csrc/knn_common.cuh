@@ -55,10 +55,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
     while (!ok) {
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
             "selp.u32 %0, 1, 0, p;\n\t}"
             : "=r"(ok)
-            : "r"(a), "r"(parity)
+            : "r"(a), "r"(parity), "r"(0x989680u)   // suspend-time hint: sleep until the phase flips
             : "memory");
     }
 }
@@ -435,6 +435,37 @@ __device__ __forceinline__ uint64_t select_pairs(uint64_t* rb, uint32_t cnt, uin
     __syncwarp();
     *kept = base;
     return P;
+}
+
+// Union of two candidate lists: selected down to the keys <= the L-th smallest key in shared
+// memory first (ties kept), then sorted by (dist, id) with dist = |a_i|^2 + key; first L written
+// (sentinel / +inf padding).  sortbuf holds SORT_MAX words; c0 + c1 <= SORT_MAX.
+template <int EPL_S>
+__device__ void finish_union(const uint64_t* b0, uint32_t c0, const uint64_t* b1, uint32_t c1, uint32_t L,
+                             uint64_t* sortbuf, float na, uint32_t* out_ids, float* out_d, uint32_t lane) {
+    uint32_t cnt = c0 + c1;
+    for (uint32_t p = lane; p < cnt; p += 32) sortbuf[p] = p < c0 ? b0[p] : b1[p - c0];
+    __syncwarp();
+    if (cnt > L) select_keys<EPL_S>(sortbuf, cnt, L, L, lane, &cnt);
+    uint32_t np = 32;
+    while (np < cnt) np <<= 1;
+    for (uint32_t p = lane; p < np; p += 32) {
+        uint64_t w = ~0ull;
+        if (p < cnt) {
+            const uint64_t e = sortbuf[p];
+            const float dist = na + __uint_as_float((uint32_t)(e >> 32));
+            w = ((uint64_t)f2ord(dist) << 32) | (uint32_t)e;
+        }
+        sortbuf[p] = w;
+    }
+    __syncwarp();
+    warp_sort_u64(sortbuf, np, lane);
+    for (uint32_t p = lane; p < L; p += 32) {
+        const uint64_t w = sortbuf[p];
+        out_ids[p] = p < cnt ? (uint32_t)w : SG_SENT;
+        out_d[p] = p < cnt ? ord2f((uint32_t)(w >> 32)) : __int_as_float(0x7f800000);
+    }
+    __syncwarp();
 }
 
 // Merge the two column halves' survivors of one row (each <= L), sort by (dist, id) with

@@ -366,8 +366,8 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     continue;
                 }
                 const uint64_t orow = p.row_map ? p.row_map[row_o] : row_o;
-                finish_row(bb[0], cc[0], bb[1], cc[1], p.L, sortbuf, p.norm_a[row_o], p.out_ids + orow * p.L,
-                           p.out_d + orow * p.L, lane);
+                finish_union<SORT_MAX / 32>(bb[0], cc[0], bb[1], cc[1], p.L, sortbuf, p.norm_a[row_o],
+                                            p.out_ids + orow * p.L, p.out_d + orow * p.L, lane);
             }
             named_bar_sync(1, nbar);   // buffers and thresholds are reused by the next row block
             pw[5] += clk() - f0;
