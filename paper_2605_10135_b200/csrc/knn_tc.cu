@@ -225,6 +225,9 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 pw[0] += c1 - c0;
                 tc_fence_after();
                 const uint32_t tb = tl + buf * BN;
+                // the self column of some row of this block can only lie in a tile overlapping the
+                // block's own columns (or anywhere, for the fallback's explicit self columns)
+                const bool self_tile = p.self_exclude && (p.self_col || (t * BN < rb * RB + RB && rb * RB < t * BN + BN));
                 // the row threshold (possibly lowered by the other stream) for this tile
                 const float te = next_up(ord2f((uint32_t)(*(volatile unsigned long long*)&s_pair[r] >> 32)));
 #pragma unroll 1
@@ -252,7 +255,6 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                         }
                         continue;
                     }
-                    const uint32_t id0 = p.col_map ? __ldg(p.col_map + col0 + lane) : col0 + lane;
                     // pass mask: bit j set iff key(j) < te, i.e. key(j) <= thr
                     uint32_t mq[4] = {0, 0, 0, 0};
 #pragma unroll
@@ -267,12 +269,12 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                         }
                     }
                     uint32_t m = mq[0] | (mq[1] << 8) | (mq[2] << 16) | (mq[3] << 24);
-                    if (scol - col0 < 32u) m &= ~(1u << (scol - col0));   // self column
+                    if (self_tile && scol - col0 < 32u) m &= ~(1u << (scol - col0));   // self column
                     c1 = clk();
                     pw[3] += c1 - c0;
                     if (p.abl & 1) m = 0;
                     if (__any_sync(0xffffffffu, m != 0)) {
-                        sids[lane] = id0;
+                        sids[lane] = p.col_map ? __ldg(p.col_map + col0 + lane) : col0 + lane;
                         float4* st4 = (float4*)(skeys + lane * KSTRIDE);
 #pragma unroll
                         for (int j4 = 0; j4 < 8; j4++)
