@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(PW * 32) prune_kernel(const uint32_t* __restri
     extern __shared__ __align__(16) uint8_t sm[];
     const uint32_t w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
-    constexpr size_t PER = NB * 32 + NB * 8 + NB * 4 + STASH * 4 + STASH + 16 + 128 + LP * 4 * 2 + (LP + 1) * 4 + QCAP * 5;
+    constexpr size_t PER = NB * 32 + NB * 8 + NB * 4 + STASH * 4 + STASH + 16 + 128 + LP * 4 * 2 + (LP + 1) * 4 + 8 + QCAP * 8;
     uint8_t* base = sm + (size_t)w * ((PER + 15) / 16 * 16);
     uint32_t* bkeys = (uint32_t*)base;                 // [NB][8]
     uint8_t* branks = base + NB * 32;                  // [NB][8]
@@ -83,8 +83,7 @@ __global__ void __launch_bounds__(PW * 32) prune_kernel(const uint32_t* __restri
     uint32_t* cnt = bloom + 32;                        // detour count per rank
     uint32_t* na = cnt + LP;                           // N[a]
     uint32_t* off = na + LP;                           // counting-sort offsets per count value (L + 1)
-    uint32_t* qb = off + LP + 1;                       // lookup queue: 2-hop ids
-    uint8_t* qm = (uint8_t*)(qb + QCAP);               // and their max(r_ad, r_db)
+    uint64_t* qe = (uint64_t*)(((uintptr_t)(off + LP + 1) + 7) & ~(uintptr_t)7);   // queue: max(r_ad, r_db) << 32 | id
     const uint64_t nwarps = (uint64_t)gridDim.x * PW;
     for (uint64_t a = (uint64_t)blockIdx.x * PW + w; a < m; a += nwarps) {
         const uint32_t* Na = knn + a * L;
@@ -99,8 +98,7 @@ __global__ void __launch_bounds__(PW * 32) prune_kernel(const uint32_t* __restri
             const uint32_t id = na[r];
             if (id == SG_SENT) continue;
             const uint32_t h = hslot(id, NBB);
-            const uint32_t fb = (id * 0x9E3779B1u >> 10) & 1023u;
-            atomicOr(&bloom[fb >> 5], 1u << (fb & 31));
+            atomicOr(&bloom[(id >> 5) & 31u], 1u << (id & 31u));   // filter bit = id mod 1024
             const uint32_t slot = atomicAdd(&bfill[h], 1u);
             if (slot < 8) {
                 bkeys[h * 8 + slot] = id;
@@ -142,26 +140,24 @@ __global__ void __launch_bounds__(PW * 32) prune_kernel(const uint32_t* __restri
                         const uint32_t b = bv[u][q];
                         const uint32_t r_db = q * 32 + lane;
                         // only ranks r_ab > max(r_ad, r_db) (rule P) / > r_ad (rule 1) can count
-                        const uint32_t mx = rule == 0 ? max(r_ad, r_db) : r_ad;
-                        const uint32_t fb = (b * 0x9E3779B1u >> 10) & 1023u;
-                        const uint32_t fw = __shfl_sync(0xffffffffu, fword, fb >> 5);
-                        // SENT never matches a slot; a is not in N[a] (self excluded), so neither
-                        // needs a test here
-                        const bool pos = (fw >> (fb & 31)) & 1u;
+                        // filter bit b mod 1024 (local ids are unordered in space); SENT never
+                        // matches a slot and a is not in N[a], so neither needs a test here
+                        const uint32_t fw = __shfl_sync(0xffffffffu, fword, (b >> 5) & 31u);
+                        const bool pos = __funnelshift_r(fw, fw, b) & 1u;
                         const uint32_t bal = __ballot_sync(0xffffffffu, pos);
                         if (pos) {
-                            const uint32_t i = qn + __popc(bal & lt);
-                            qb[i] = b;
-                            qm[i] = (uint8_t)mx;
+                            const uint32_t mx = rule == 0 ? max(r_ad, r_db) : r_ad;
+                            qe[qn + __popc(bal & lt)] = ((uint64_t)mx << 32) | b;
                         }
                         qn += __popc(bal);
                     }
                     if ((u + 1) % FLUSH == 0) {
                         __syncwarp();
                         for (uint32_t i = lane; i < qn; i += 32) {
-                            const uint32_t b = qb[i];
+                            const uint64_t e = qe[i];
+                            const uint32_t b = (uint32_t)e;
                             const uint32_t r_ab = lookup<NB, NBB>((const uint4*)bkeys, (const uint2*)branks, sk, sr, nstash, b);
-                            if (r_ab != 0xFFFFFFFFu && qm[i] < r_ab) atomicAdd(&cnt[r_ab], 1u);
+                            if (r_ab != 0xFFFFFFFFu && (uint32_t)(e >> 32) < r_ab) atomicAdd(&cnt[r_ab], 1u);
                         }
                         __syncwarp();
                         qn = 0;
@@ -221,7 +217,7 @@ __global__ void __launch_bounds__(PW * 32) prune_kernel(const uint32_t* __restri
 template <int LPL, int PW>
 size_t prune_smem() {
     constexpr uint32_t LP = LPL * 32, NB = LP / 2;
-    constexpr size_t PER = NB * 32 + NB * 8 + NB * 4 + STASH * 4 + STASH + 16 + 128 + LP * 4 * 2 + (LP + 1) * 4 + QCAP * 5;
+    constexpr size_t PER = NB * 32 + NB * 8 + NB * 4 + STASH * 4 + STASH + 16 + 128 + LP * 4 * 2 + (LP + 1) * 4 + 8 + QCAP * 8;
     return (size_t)PW * ((PER + 15) / 16 * 16) + 64;
 }
 
