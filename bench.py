@@ -272,11 +272,14 @@ def main():
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
+        outh = None
         for _ in range(args.steps):
             xd = xh.to("cuda", non_blocking=True)
             ix = step(xd)
-            out = ix.merged.cpu()
-            d2h = out.numel() * out.element_size()
+            if outh is None:   # pinned host buffer for the merged graph (allocated once, untimed cost)
+                outh = torch.empty(ix.merged.shape, dtype=ix.merged.dtype, pin_memory=True)
+            outh.copy_(ix.merged, non_blocking=True)
+            d2h = outh.numel() * outh.element_size()
         e1.record()
         torch.cuda.synchronize()
         barrier()

@@ -230,6 +230,15 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 const bool self_tile = p.self_exclude && (p.self_col || (t * BN < rb * RB + RB && rb * RB < t * BN + BN));
                 // the row threshold (possibly lowered by the other stream) for this tile
                 const float te = next_up(ord2f((uint32_t)(*(volatile unsigned long long*)&s_pair[r] >> 32)));
+                // compaction target rank per stream for this tile: L, or (extrapolated) the rank for
+                // the fraction of columns seen; trigger: buffer full, or `eager` above the target
+                uint32_t want = p.L, kmax = keep_max, trig = C - 32;
+                if (p.alpha100) {
+                    const float f = (float)((ti + 1) * BN) / (float)p.mb;
+                    const uint32_t rr = (uint32_t)(p.alpha100 * 0.005f * (float)p.L * f) + p.beta;
+                    if (rr < p.L) { want = rr; kmax = want + (C - 32 - want) / 8; }
+                    if (want + p.eager < trig) trig = want + p.eager;
+                }
 #pragma unroll 1
                 for (uint32_t hp = s * (BN / 64); hp < (s + 1) * (BN / 64); hp++) {   // this stream's passes
                     uint32_t v[32];
@@ -303,14 +312,10 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     // make room: compact rows whose buffer cannot take another pass to the target
                     // rank per stream (L, or the extrapolated rank for the fraction seen) under the
                     // row threshold, and lower the shared pair
-                    uint32_t need = __ballot_sync(0xffffffffu, cnt > C - 32);
+                    // (extrapolated mode: also eagerly, once a stream holds `eager` entries above its
+                    // target rank, so the shared threshold follows the fraction of columns seen)
+                    uint32_t need = __ballot_sync(0xffffffffu, cnt > trig);
                     if (need) {
-                        uint32_t want = p.L, kmax = keep_max;
-                        if (p.alpha100) {
-                            const uint64_t seen = (uint64_t)ti * BN + (hp + 1) * 32;
-                            const uint64_t rr = (uint64_t)p.alpha100 * p.L * seen / (200ull * p.mb) + p.beta;
-                            if (rr < p.L) { want = (uint32_t)rr; kmax = want + (C - 32 - want) / 8; }
-                        }
                         do {
                             const int o = __ffs(need) - 1;
                             need &= need - 1;
@@ -546,7 +551,7 @@ sg_status knn_core(const Operand& A, const Operand& B, int /*metric*/, bool self
     static const int tb = env_int("SG_TBACK", 8), ne = env_int("SG_KNN_NOEPI", 0), nl = env_int("SG_KNN_NOLOAD", 0),
                      ab = env_int("SG_KNN_ABL", 0), alpha = env_int("SG_KNN_ALPHA", 150),
                      beta = env_int("SG_KNN_BETA", -1), report = env_int("SG_KNN_REPORT", 0),
-                     eager = env_int("SG_KNN_EAGER", 16);
+                     eager = env_int("SG_KNN_EAGER", -1);
     p.t_back = (uint32_t)tb;
     const bool main_sweep = L > 1 && !probe;          // not the spatial-order assignment pass
     p.noepi = ne && main_sweep;
@@ -567,7 +572,7 @@ sg_status knn_core(const Operand& A, const Operand& B, int /*metric*/, bool self
     SG_CUDA(cudaMemsetAsync(fail_count, 0, sizeof(uint32_t), st));
     p.alpha100 = (uint32_t)alpha;
     p.beta = (uint32_t)(beta >= 0 ? beta : tr ? 6 : 12);   // per column stream
-    p.eager = (uint32_t)eager;
+    p.eager = (uint32_t)(eager >= 0 ? eager : tr ? 16 : 64);
     p.fail_count = fail_count;
     p.fail_rows = fail_rows;
     SG_TRY(launch_knn(A, B, p, st));

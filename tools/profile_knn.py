@@ -40,18 +40,20 @@ def main():
     torch.cuda.synchronize()
     ms, nl, _ = api.scalegann_stats_read(reset=True)
     if a.prof:
-        cnt = torch.zeros(80, dtype=torch.int64, device="cuda")
+        NW = 18   # warps per CTA of the row-major kernel (producer, MMA, 16 epilogue)
+        cnt = torch.zeros(NW * 8, dtype=torch.int64, device="cuda")
         api.scalegann_knn_profile(cnt)
         api.scalegann_knn(x, a.L, precision=a.precision, ws=ws)
         torch.cuda.synchronize()
         api.scalegann_knn_profile(None)
-        c = cnt.view(10, 8).double().cpu()
+        c = cnt.view(NW, 8).double().cpu()
         names = ["wait", "tmem/full", "compact", "mask", "insert", "final"]
-        for w in range(10):
+        for w in range(NW):
             print(f"warp {w}: " + " ".join(f"{n}={v / 1e9:.2f}G" for n, v in zip(names, c[w, :6].tolist())))
-        ins = c[2:, 6].sum().item() * 32 / 32   # lane-0 sums of its own row only
-        print(f"insertions (lane-0 rows) per row: {c[2:, 6].sum().item() / (8 * 148 * max(1, (a.m // 256) // 148)):.1f}"
-              f"  loop iterations per warp-row-block: {c[2:, 7].sum().item() / (8 * 148 * max(1, (a.m // 256) // 148)):.1f}")
+        # counters are lane-0 sums: lane 0 of each (q, a, stream) warp = one row's insertions per stream
+        nrb = a.m / 256.0
+        print(f"insertions per row (both streams): {c[2:, 6].sum().item() / (8 * nrb):.1f}"
+              f"  insertion-loop iterations per warp-row-block: {c[2:, 7].sum().item() / (16 * nrb):.1f}")
     per = ms / a.reps   # per call (spatial-order pass + main sweep)
     fl = 2.0 * a.m * a.m * a.d
     print(json.dumps({"m": a.m, "d": a.d, "L": a.L, "ms_per_launch": per, "tflops": fl / (per / 1e3) / 1e12}))
