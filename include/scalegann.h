@@ -138,8 +138,10 @@ sg_status scalegann_entry_points(const uint32_t* home, const float* primary_d, u
  * -a.b (IP), distance tiles on tcgen05 tensor cores with fp32 accumulation and
  * a fused per-row top-L.  ids/dists out: ma x L, rows sorted by (dist, id),
  * padded with (SENTINEL, +inf) when fewer than L candidates exist.
- * Limits: L <= 256; d*operand_bytes <= 768 (d <= 384 for F16_EXACT, 192 for
- * TF32, 64 for TF32X3), ma, mb < 2^31. */
+ * Limits: L <= 256; ma, mb < 2^31; up to 128 operand atoms of 128 bytes per row
+ * (d <= 8176 F16_EXACT, 4088 TF32, 1362 TF32X3).  Rows up to 4 atoms (d <= 248
+ * F16_EXACT with L2) keep the CTA's row block resident in shared memory; wider rows
+ * stream both operands through the ring (slower per flop, same results). */
 sg_status scalegann_knn_workspace(uint64_t ma, uint64_t mb, uint32_t d, sg_dtype dtype, uint32_t L,
                                   int32_t precision, size_t* bytes);
 sg_status scalegann_knn(const void* xa, const uint32_t* ida, uint64_t ma, const void* xb,

@@ -107,8 +107,8 @@ static int worst_prec(sg_dtype dtype, int32_t precision) {
 static sg_status check_knn_shape(int prec, int metric, uint32_t d, uint32_t L) {
     SG_CHECK_ARG(L >= 1 && L <= 256, "kNN: L must be in [1, 256]");
     const uint32_t nf = knn_full_atoms(prec, metric, d);
-    if (nf > 4) {
-        set_error("kNN: d=%u needs %u 128-byte operand atoms per row with this precision (max 4)", d, nf);
+    if (nf > 128) {   // > 4 atoms: streamed-A kernel (knn_tc.cu); the bound only caps d
+        set_error("kNN: d=%u needs %u 128-byte operand atoms per row with this precision (max 128)", d, nf);
         return SG_ERR_UNSUPPORTED;
     }
     return SG_OK;

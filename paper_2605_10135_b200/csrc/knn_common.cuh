@@ -162,6 +162,7 @@ struct KnnParams {
     const uint32_t* col_map;   // B row (operand order) -> reported id (nullptr = identity)
     uint32_t ma, mb, L, C, n_rb, n_ct, stages;
     uint32_t keep_max;         // in-loop compaction keeps between L and keep_max candidates
+    uint32_t nka;              // streamed-A kernel: full 128-byte K atoms per row (run time)
     // Extrapolated thresholds (columns in id order, no rotation): after `seen` of mb columns the
     // in-loop compaction keeps rank r = min(L, alpha100 * L * seen / (100 mb) + beta) instead of L.
     // The buffer always holds every seen column with (key, id) <= the threshold entry, so a row

@@ -39,19 +39,24 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     constexpr uint32_t EL = KIND ? 4 : 2;                  // bytes per element
     constexpr uint32_t ATOM_K = 128 / EL;                  // elements per 128B atom
-    constexpr uint32_t NSLOT = NKA + MINI;                 // ring slots per column tile
-    // f16 operands: A lives in TMEM (read once per row block), so the tensor core streams only
-    // B from shared memory; tf32 (wider A) keeps A in shared memory.
-    constexpr uint32_t NACC = KIND == 0 ? NACC_MAX : 1;   // tf32 A halves do not both fit in smem
+    // NKA == 0: streamed-A mode for wide operands (A does not fit in shared memory): every ring
+    // slot carries one K atom of B (column tile) and of A (128-row block), the atom count is read
+    // at run time (p.nka), one 128-row accumulator
+    constexpr bool SA = NKA == 0;
+    const uint32_t nka = SA ? p.nka : (uint32_t)NKA;
+    const uint32_t nslot = nka + MINI;                     // ring slots per column tile
+    constexpr uint32_t SLOTB = SA ? 2 * SLOT : SLOT;       // ring slot bytes (B atom | A atom)
+    // f16 operands keep both 128-row halves of A resident; tf32 (wider A) keeps one
+    constexpr uint32_t NACC = (KIND == 0 && !SA) ? NACC_MAX : 1;
     constexpr uint32_t RB = MSUB * NACC;                  // rows per row block of this instantiation
     constexpr bool ATM = KIND == 0 && SG_ATM;
     constexpr uint32_t NBUF = ATM ? 2 : 512 / (NACC * BN);
-    constexpr uint32_t AHALF = ATM ? 0u : NKA * ATOM + (MINI ? MINIB : 0u);   // smem bytes of one 128-row half
+    constexpr uint32_t AHALF = (ATM || SA) ? 0u : NKA * ATOM + (MINI ? MINIB : 0u);   // smem bytes of one resident half
     // offsets from smem_raw (not integer casts) so the compiler keeps shared-space accesses (LDS/STS)
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sA = smem;                                    // [NACC][NKA atoms + mini] (SS mode)
     uint8_t* sB = smem + NACC * AHALF;
-    Bars* bars = (Bars*)(sB + p.stages * SLOT);
+    Bars* bars = (Bars*)(sB + p.stages * SLOTB);
     uint8_t* bars_end = (uint8_t*)(bars + 1);
     unsigned long long* s_pair = (unsigned long long*)(bars_end + ((128u - (smem_u32(bars_end) & 127u)) & 127u));
     uint32_t (*s_cnt)[BM] = (uint32_t (*)[BM])(s_pair + BM);          // [2][BM] stream counts
@@ -96,11 +101,11 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         if (lane == 0) {
             uint32_t stage = 0, sph = 0, it = 0;
             for (uint32_t rb = blockIdx.x; rb < n_rb; rb += gridDim.x, it++) {
-                if (!ATM) {
+                if (!ATM && !SA) {
                     if (it > 0) mbar_wait(&bars->a_empty, (it - 1) & 1);
                     mbar_expect_tx(&bars->a_full, NACC * AHALF);
                 }
-                for (uint32_t a = 0; a < NACC && !ATM; a++) {
+                for (uint32_t a = 0; a < NACC && !ATM && !SA; a++) {
                     uint8_t* base = sA + a * AHALF;
                     for (int ka = 0; ka < NKA; ka++)
                         tma_load_2d(&tmA, &bars->a_full, base + ka * ATOM, ka * ATOM_K, rb * RB + a * MSUB);
@@ -109,16 +114,19 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 for (uint32_t ti = 0, t = tile_at(p, rb, 0); ti < p.n_ct; ti++, t = t + 1 == p.n_ct ? 0 : t + 1) {
                     long long w0 = clk();
 #pragma unroll
-                    for (uint32_t ka = 0; ka < NSLOT; ka++) {
+                    for (uint32_t ka = 0; ka < nslot; ka++) {
                         mbar_wait(&bars->empty[stage], sph ^ 1);
+                        uint8_t* slot = sB + stage * SLOTB;
                         if (p.noload) {
                             mbar_arrive(&bars->full[stage]);
-                        } else if (ka < NKA) {
-                            mbar_expect_tx(&bars->full[stage], BATOM);
-                            tma_load_2d(&tmB, &bars->full[stage], sB + stage * SLOT, ka * ATOM_K, t * BN);
+                        } else if (ka < nka) {
+                            mbar_expect_tx(&bars->full[stage], SA ? BATOM + ATOM : BATOM);
+                            tma_load_2d(&tmB, &bars->full[stage], slot, ka * ATOM_K, t * BN);
+                            if (SA) tma_load_2d(&tmA, &bars->full[stage], slot + SLOT, ka * ATOM_K, rb * RB);
                         } else {
-                            mbar_expect_tx(&bars->full[stage], BMINI);
-                            tma_load_2d(&tmBm, &bars->full[stage], sB + stage * SLOT, NKA * ATOM_K, t * BN);
+                            mbar_expect_tx(&bars->full[stage], SA ? BMINI + MINIB : BMINI);
+                            tma_load_2d(&tmBm, &bars->full[stage], slot, nka * ATOM_K, t * BN);
+                            if (SA) tma_load_2d(&tmAm, &bars->full[stage], slot + SLOT, nka * ATOM_K, rb * RB);
                         }
                         if (++stage == p.stages) { stage = 0; sph ^= 1; }
                     }
@@ -133,7 +141,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
             uint32_t stage = 0, sph = 0, it = 0, git = 0;
             for (uint32_t rb = blockIdx.x; rb < n_rb; rb += gridDim.x, it++) {
-                mbar_wait(&bars->a_full, it & 1);
+                if (!SA) mbar_wait(&bars->a_full, it & 1);
                 tc_fence_after();
                 for (uint32_t ti = 0; ti < p.n_ct; ti++, git++) {
                     const uint32_t buf = git % NBUF;
@@ -142,12 +150,12 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     pw[0] += clk() - w0;
                     tc_fence_after();
 #pragma unroll
-                    for (uint32_t ka = 0; ka < NSLOT; ka++) {
+                    for (uint32_t ka = 0; ka < nslot; ka++) {
                         const long long w1 = clk();
                         mbar_wait(&bars->full[stage], sph);
                         pw[1] += clk() - w1;
                         tc_fence_after();
-                        const uint32_t bslot = b_base + stage * SLOT;
+                        const uint32_t bslot = b_base + stage * SLOTB;
 #pragma unroll
                         for (uint32_t a = 0; a < NACC; a++) {
                             const uint32_t dcol = tmem + (a * NBUF + buf) * BN;
@@ -161,6 +169,16 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                                                   (ka | kk) != 0);
                                 } else {
                                     tc_mma_ts(dcol, at + NKA * 32, desc_sw32(bslot), idesc, NKA != 0);
+                                }
+                            } else if constexpr (SA) {
+                                const uint32_t aslot = bslot + SLOT;   // this K atom of A
+                                if (ka < nka) {
+#pragma unroll
+                                    for (uint32_t kk = 0; kk < 4; kk++)
+                                        tc_mma<KIND>(dcol, desc_sw128(aslot + kk * 32), desc_sw128(bslot + kk * 32), idesc,
+                                                     (ka | kk) != 0);
+                                } else {
+                                    tc_mma<KIND>(dcol, desc_sw32(aslot), desc_sw32(bslot), idesc, nka != 0);
                                 }
                             } else {
                                 if (ka < NKA) {
@@ -178,7 +196,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     }
                     tc_commit(&bars->tm_full[buf]);
                 }
-                if (!ATM) tc_commit(&bars->a_empty);
+                if (!ATM && !SA) tc_commit(&bars->a_empty);
             }
         }
     } else {
@@ -409,15 +427,18 @@ uint32_t keep_target(uint32_t L, uint32_t C) {
 
 template <int KIND, int NKA, int MINI, int EPL>
 sg_status launch_t(const CUtensorMap* maps, KnnParams& p, cudaStream_t st) {
-    constexpr uint32_t AHALF = (KIND == 0 && SG_ATM) ? 0u : NKA * ATOM + (MINI ? MINIB : 0u);   // A in TMEM for f16
-    constexpr uint32_t NACC = KIND == 0 ? NACC_MAX : 1;
+    constexpr bool SA = NKA == 0;
+    constexpr uint32_t AHALF = ((KIND == 0 && SG_ATM) || SA) ? 0u : NKA * ATOM + (MINI ? MINIB : 0u);
+    constexpr uint32_t NACC = (KIND == 0 && !SA) ? NACC_MAX : 1;
+    constexpr uint32_t SLOTB = SA ? 2 * SLOT : SLOT;
     const size_t fixed = NACC * AHALF + sizeof(Bars) + 128 + BM * 8 + 2 * BM * 4 + 8 * NACC * SCRATCH + 1024 + 64;
     const size_t budget = 227 * 1024;
-    if (fixed + (NKA + MINI) * SLOT > budget) { set_error("kNN: operand too wide for shared memory"); return SG_ERR_UNSUPPORTED; }
-    uint32_t stages = (uint32_t)((budget - fixed) / SLOT);
+    const size_t min_slots = SA ? 2 : NKA + MINI;
+    if (fixed + min_slots * SLOTB > budget) { set_error("kNN: operand too wide for shared memory"); return SG_ERR_UNSUPPORTED; }
+    uint32_t stages = (uint32_t)((budget - fixed) / SLOTB);
     if (stages > MAX_STAGES) stages = MAX_STAGES;
     p.stages = stages;
-    const size_t smem = fixed + stages * SLOT;
+    const size_t smem = fixed + stages * SLOTB;
     auto kern = knn_tc_kernel<KIND, NKA, MINI, EPL>;
     SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const uint32_t grid = p.n_rb < (uint32_t)num_sms() ? p.n_rb : (uint32_t)num_sms();
@@ -430,14 +451,17 @@ sg_status launch_t(const CUtensorMap* maps, KnnParams& p, cudaStream_t st) {
 
 template <int KIND, int MINI, int EPL>
 sg_status launch_nka(int nka, const CUtensorMap* maps, KnnParams& p, cudaStream_t st) {
+    // resident-A kernel when the row block fits in shared memory, else streamed A (any width)
+    sg_status r = SG_ERR_UNSUPPORTED;
     switch (nka) {
-        case 1: return launch_t<KIND, 1, MINI, EPL>(maps, p, st);
-        case 2: return launch_t<KIND, 2, MINI, EPL>(maps, p, st);
-        case 3: return launch_t<KIND, 3, MINI, EPL>(maps, p, st);
-        case 4: return launch_t<KIND, 4, MINI, EPL>(maps, p, st);
+        case 1: r = launch_t<KIND, 1, MINI, EPL>(maps, p, st); break;
+        case 2: r = launch_t<KIND, 2, MINI, EPL>(maps, p, st); break;
+        case 3: r = launch_t<KIND, 3, MINI, EPL>(maps, p, st); break;
+        case 4: r = launch_t<KIND, 4, MINI, EPL>(maps, p, st); break;
     }
-    set_error("kNN: unsupported operand width (%d atoms; max 4 per 128-row half)", nka);
-    return SG_ERR_UNSUPPORTED;
+    if (r != SG_ERR_UNSUPPORTED) return r;
+    p.nka = (uint32_t)nka;
+    return launch_t<KIND, 0, MINI, EPL>(maps, p, st);
 }
 
 template <int KIND, int EPL>
@@ -506,7 +530,7 @@ sg_status launch_knn(const Operand& A, const Operand& B, KnnParams& p, cudaStrea
     }
     const int epl = (int)(p.C / 32);
     const int nka = (int)A.nfull, mini = (int)A.mini;
-    if (use_transposed(p.L)) return launch_knn_t(maps, p, (int)A.esize, nka, mini, st);
+    if (use_transposed(p.L) && nka <= 4) return launch_knn_t(maps, p, (int)A.esize, nka, mini, st);
     if (A.esize == 4) {
         if (epl <= 8) return launch_mini<1, 8>(nka, mini, maps, p, st);
         if (epl <= 16) return launch_mini<1, 16>(nka, mini, maps, p, st);

@@ -313,3 +313,33 @@ def test_end_to_end_c0_recall(api, oracle_mod):
     res_g, _, _ = oracle_mod.search(x.numpy(), u32(idx.merged), idx.entry, q.numpy(), topk=10, beam=64)
     ro, rg = oracle_mod.recall(res_o, gt), oracle_mod.recall(res_g, gt)
     assert abs(ro - rg) <= 0.005, (ro, rg)
+
+
+# ------------------------------------------------------------------ a5 wide rows (streamed-A kernel)
+@pytest.mark.parametrize("d", [512, 300])
+def test_knn_wide_integer_exact(api, oracle_mod, d):
+    """d * 2 bytes beyond 4 resident atoms: both operands stream through the ring; integer data
+    with 2 d max^2 < 2^24 stays F16_EXACT, so ids and dists are bit-identical to the oracle."""
+    x = torch.clamp(torch.round(datagen.sift_like(1400, d, seed=d) / 4), 0, 60)
+    ids, dd = api.scalegann_knn(x.cuda(), 64)
+    oi, od = oracle_mod.knn(x.numpy(), 64)
+    assert np.array_equal(u32(ids), oi) and np.array_equal(dd.cpu().numpy(), od)
+
+
+def test_knn_c3_text_embedding_768(api, oracle_mod):
+    """C3-shaped rows (768-d, power-law spectrum, L2-normalised): TF32 operands,
+    fp32 accumulation, judged by the P4 tolerance rule."""
+    x = datagen.mixture(1200, 768, 1.0, seed=31, normalise=True)
+    ids, dd = api.scalegann_knn(x.cuda(), 64)
+    oi, od = oracle_mod.knn(x.numpy(), 64)
+    fails, msg = check_knn(u32(ids), dd.cpu().numpy(), oi, od, x.numpy())
+    assert fails == 0, msg
+
+
+def test_knn_c2_deep_96(api, oracle_mod):
+    """C2-shaped rows (96-d, spectrum beta 0.7, L2-normalised): TF32, tolerance rule."""
+    x = datagen.mixture(2000, 96, 0.7, seed=32, normalise=True)
+    ids, dd = api.scalegann_knn(x.cuda(), 128)
+    oi, od = oracle_mod.knn(x.numpy(), 128)
+    fails, msg = check_knn(u32(ids), dd.cpu().numpy(), oi, od, x.numpy())
+    assert fails == 0, msg
