@@ -59,14 +59,14 @@ __device__ __forceinline__ void load_rows(const uint32_t* __restrict__ knn, cons
     }
 }
 
-template <int LPL, int PW>   // ranks per lane = L_pad / 32; warps (nodes) per CTA
+template <int LPL, int PW, int RULE>   // ranks per lane = L_pad / 32; warps (nodes) per CTA; prune rule
 __global__ void __launch_bounds__(PW * 32) prune_kernel(const uint32_t* __restrict__ knn, const float* __restrict__ knn_d,
                                                         uint64_t m, uint32_t L, uint32_t R, uint32_t rule,
                                                         uint32_t* __restrict__ out, float* __restrict__ out_d) {
     constexpr uint32_t LP = LPL * 32;          // padded L (power of two)
     constexpr uint32_t NB = LP / 2;            // buckets of 8 slots: load factor 1/4
     constexpr uint32_t NBB = LPL == 1 ? 4 : LPL == 2 ? 5 : LPL == 4 ? 6 : 7;
-    constexpr uint32_t FLUSH = QCAP / (32 * LPL) < 4 ? QCAP / (32 * LPL) : 4;   // rows per queue flush
+    constexpr int FLUSH = QCAP / (32 * LPL) < 4 ? QCAP / (32 * LPL) : 4;   // rows per queue flush
     static_assert((1u << NBB) == NB, "bucket bits");
     extern __shared__ __align__(16) uint8_t sm[];
     const uint32_t w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(PW * 32) prune_kernel(const uint32_t* __restri
                 for (uint32_t rdb = lane; rdb < L; rdb += 32) {
                     const uint32_t b = __ldg(knn + (uint64_t)dl * L + rdb);
                     if (b == SG_SENT || b == (uint32_t)a) continue;
-                    const uint32_t mx = rule == 0 ? max(r0, rdb) : r0;
+                    const uint32_t mx = RULE == 0 ? max(r0, rdb) : r0;
                     for (uint32_t r = mx + 1; r < L; r++)
                         if (na[r] == b) { atomicAdd(&cnt[r], 1u); break; }
                 }
@@ -131,37 +131,48 @@ __global__ void __launch_bounds__(PW * 32) prune_kernel(const uint32_t* __restri
             load_rows<LPL>(knn, na, 0, L, lane, bv);
             for (uint32_t r0 = 0; r0 < L; r0 += 4) {
                 if (r0 + 4 < L) load_rows<LPL>(knn, na, r0 + 4, L, lane, bn);
-                uint32_t qn = 0;
 #pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    const uint32_t r_ad = r0 + u;
+                for (int u0 = 0; u0 < 4; u0 += FLUSH) {
+                    // (1) filter FLUSH rows x LPL ids per lane into a local bit mask
+                    uint32_t lm = 0;
 #pragma unroll
-                    for (int q = 0; q < LPL; q++) {
-                        const uint32_t b = bv[u][q];
-                        const uint32_t r_db = q * 32 + lane;
-                        // only ranks r_ab > max(r_ad, r_db) (rule P) / > r_ad (rule 1) can count
-                        // filter bit b mod 1024 (local ids are unordered in space); SENT never
-                        // matches a slot and a is not in N[a], so neither needs a test here
-                        const uint32_t fw = __shfl_sync(0xffffffffu, fword, (b >> 5) & 31u);
-                        const bool pos = __funnelshift_r(fw, fw, b) & 1u;
-                        const uint32_t bal = __ballot_sync(0xffffffffu, pos);
-                        if (pos) {
-                            const uint32_t mx = rule == 0 ? max(r_ad, r_db) : r_ad;
-                            qe[qn + __popc(bal & lt)] = ((uint64_t)mx << 32) | b;
+                    for (int u = u0; u < u0 + FLUSH; u++)
+#pragma unroll
+                        for (int q = 0; q < LPL; q++) {
+                            const uint32_t b = bv[u][q];
+                            const uint32_t fw = __shfl_sync(0xffffffffu, fword, (b >> 5) & 31u);
+                            lm |= (__funnelshift_r(fw, fw, b) & 1u) << ((u - u0) * LPL + q);
                         }
-                        qn += __popc(bal);
+                    // (2) queue offsets: exclusive warp scan of the positives per lane
+                    const uint32_t np = __popc(lm);
+                    uint32_t inc = np;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+                        if (lane >= (uint32_t)o) inc += t;
                     }
-                    if ((u + 1) % FLUSH == 0) {
-                        __syncwarp();
-                        for (uint32_t i = lane; i < qn; i += 32) {
-                            const uint64_t e = qe[i];
-                            const uint32_t b = (uint32_t)e;
-                            const uint32_t r_ab = lookup<NB, NBB>((const uint4*)bkeys, (const uint2*)branks, sk, sr, nstash, b);
-                            if (r_ab != 0xFFFFFFFFu && (uint32_t)(e >> 32) < r_ab) atomicAdd(&cnt[r_ab], 1u);
-                        }
-                        __syncwarp();
-                        qn = 0;
+                    const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+                    uint32_t pos = inc - np;
+                    // (3) append (max(r_ad, r_db) << 32 | id) of the positives, fixed order
+#pragma unroll
+                    for (int u = u0; u < u0 + FLUSH; u++)
+#pragma unroll
+                        for (int q = 0; q < LPL; q++)
+                            if ((lm >> ((u - u0) * LPL + q)) & 1u) {
+                                // only ranks r_ab > max(r_ad, r_db) (rule P) / > r_ad (rule 1) count
+                                const uint32_t r_ad = r0 + u, r_db = q * 32 + lane;
+                                const uint32_t mx = RULE == 0 ? max(r_ad, r_db) : r_ad;
+                                qe[pos++] = ((uint64_t)mx << 32) | bv[u][q];
+                            }
+                    __syncwarp();
+                    // (4) resolve the queue densely against the table
+                    for (uint32_t i = lane; i < total; i += 32) {
+                        const uint64_t e = qe[i];
+                        const uint32_t b = (uint32_t)e;
+                        const uint32_t r_ab = lookup<NB, NBB>((const uint4*)bkeys, (const uint2*)branks, sk, sr, nstash, b);
+                        if (r_ab != 0xFFFFFFFFu && (uint32_t)(e >> 32) < r_ab) atomicAdd(&cnt[r_ab], 1u);
                     }
+                    __syncwarp();
                 }
 #pragma unroll
                 for (int u = 0; u < 4; u++)
@@ -221,11 +232,11 @@ size_t prune_smem() {
     return (size_t)PW * ((PER + 15) / 16 * 16) + 64;
 }
 
-template <int LPL, int PW>
+template <int LPL, int PW, int RULE>
 sg_status prune_launch(const uint32_t* knn, const float* knn_d, uint64_t m, uint32_t L, uint32_t R, uint32_t rule,
                        uint32_t* out, float* out_d, cudaStream_t st) {
     const size_t smem = prune_smem<LPL, PW>();
-    auto kern = prune_kernel<LPL, PW>;
+    auto kern = prune_kernel<LPL, PW, RULE>;
     SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PW * 32, smem));
@@ -242,10 +253,16 @@ sg_status prune_launch(const uint32_t* knn, const float* knn_d, uint64_t m, uint
 sg_status launch_prune(const uint32_t* knn, const float* knn_d, uint64_t m, uint32_t L, uint32_t R, uint32_t rule,
                        uint32_t* out, float* out_d, cudaStream_t st) {
     if (m == 0) return SG_OK;
-    if (L <= 32) return prune_launch<1, 8>(knn, knn_d, m, L, R, rule, out, out_d, st);
-    if (L <= 64) return prune_launch<2, 8>(knn, knn_d, m, L, R, rule, out, out_d, st);
-    if (L <= 128) return prune_launch<4, 8>(knn, knn_d, m, L, R, rule, out, out_d, st);
-    return prune_launch<8, 4>(knn, knn_d, m, L, R, rule, out, out_d, st);
+    if (rule == 0) {
+        if (L <= 32) return prune_launch<1, 8, 0>(knn, knn_d, m, L, R, rule, out, out_d, st);
+        if (L <= 64) return prune_launch<2, 8, 0>(knn, knn_d, m, L, R, rule, out, out_d, st);
+        if (L <= 128) return prune_launch<4, 8, 0>(knn, knn_d, m, L, R, rule, out, out_d, st);
+        return prune_launch<8, 4, 0>(knn, knn_d, m, L, R, rule, out, out_d, st);
+    }
+    if (L <= 32) return prune_launch<1, 8, 1>(knn, knn_d, m, L, R, rule, out, out_d, st);
+    if (L <= 64) return prune_launch<2, 8, 1>(knn, knn_d, m, L, R, rule, out, out_d, st);
+    if (L <= 128) return prune_launch<4, 8, 1>(knn, knn_d, m, L, R, rule, out, out_d, st);
+    return prune_launch<8, 4, 1>(knn, knn_d, m, L, R, rule, out, out_d, st);
 }
 
 }  // namespace sg
