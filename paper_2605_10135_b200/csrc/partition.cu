@@ -24,17 +24,26 @@ namespace {
 constexpr int K2_THREADS = 1024;
 constexpr int KMAX = 64;
 
+// KB >= k: compile-time bound for the per-vector arrays (registers, static indexing); the
+// centroids are staged in shared memory when they fit (SMEM_C), else read through L1.
+template <int KB, bool SMEM_C>
 __global__ void __launch_bounds__(256) centroid_dist_order(const void* __restrict__ x, int dtype, uint64_t n,
                                                            uint32_t d, const float* __restrict__ C, uint32_t k,
                                                            float* __restrict__ dist, uint8_t* __restrict__ order) {
     __shared__ float tile[8][32][33];
+    extern __shared__ float sC[];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (SMEM_C) {
+        for (uint32_t e = threadIdx.x; e < k * d; e += blockDim.x) sC[e] = C[e];
+        __syncthreads();
+    }
+    const float* Cs = SMEM_C ? sC : C;
     const uint64_t v0 = ((uint64_t)blockIdx.x * 8 + warp) * 32;
     if (v0 >= n) return;
     const uint64_t v = v0 + lane;
-    float acc[KMAX];
+    float acc[KB];
 #pragma unroll
-    for (int c = 0; c < KMAX; c++) acc[c] = 0.f;
+    for (int c = 0; c < KB; c++) acc[c] = 0.f;
     for (uint32_t j0 = 0; j0 < d; j0 += 32) {
         // coalesced load of rows v0..v0+31, columns j0..j0+31 (transposed through smem)
         for (int rr = 0; rr < 32; rr++) {
@@ -47,32 +56,55 @@ __global__ void __launch_bounds__(256) centroid_dist_order(const void* __restric
         }
         __syncwarp();
         const uint32_t jn = d - j0 < 32 ? d - j0 : 32;
+        if (SMEM_C && (d & 3) == 0 && jn == 32) {
+            // 4 dimensions of this lane's vector in registers, reused by every centroid (read
+            // as one 16-byte broadcast); per (v, c) the fmaf chain stays in j order (reading R1)
+            for (uint32_t jj = 0; jj < 32; jj += 4) {
+                const float t0 = tile[warp][lane][jj], t1 = tile[warp][lane][jj + 1];
+                const float t2 = tile[warp][lane][jj + 2], t3 = tile[warp][lane][jj + 3];
 #pragma unroll
-        for (int c = 0; c < KMAX; c++) {
-            if ((uint32_t)c < k) {
-                float a = acc[c];
-                for (uint32_t jj = 0; jj < jn; jj++) {
-                    float diff = __fsub_rn(tile[warp][lane][jj], __ldg(&C[(size_t)c * d + j0 + jj]));
-                    a = __fmaf_rn(diff, diff, a);
+                for (int c = 0; c < KB; c++) {
+                    if ((uint32_t)c < k) {
+                        const float4 c4 = *(const float4*)(Cs + (size_t)c * d + j0 + jj);
+                        float a = acc[c], df;
+                        df = __fsub_rn(t0, c4.x); a = __fmaf_rn(df, df, a);
+                        df = __fsub_rn(t1, c4.y); a = __fmaf_rn(df, df, a);
+                        df = __fsub_rn(t2, c4.z); a = __fmaf_rn(df, df, a);
+                        df = __fsub_rn(t3, c4.w); a = __fmaf_rn(df, df, a);
+                        acc[c] = a;
+                    }
                 }
-                acc[c] = a;
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < KB; c++) {
+                if ((uint32_t)c < k) {
+                    float a = acc[c];
+                    const float* cc = Cs + (size_t)c * d + j0;
+                    for (uint32_t jj = 0; jj < jn; jj++) {
+                        // the fixed fp32 order of reading R1: acc = fma(diff, diff, acc), j ascending
+                        float diff = __fsub_rn(tile[warp][lane][jj], SMEM_C ? cc[jj] : __ldg(cc + jj));
+                        a = __fmaf_rn(diff, diff, a);
+                    }
+                    acc[c] = a;
+                }
             }
         }
         __syncwarp();
     }
     if (v >= n) return;
-    uint8_t ord[KMAX];
+    // preference order by (d^2, c): the rank of c is the number of (d^2, c') before it
 #pragma unroll
-    for (int c = 0; c < KMAX; c++) {
+    for (int c = 0; c < KB; c++) {
         if ((uint32_t)c < k) {
             dist[v * k + c] = acc[c];
-            // insertion by (d, c): stable because c increases
-            int j = c;
-            while (j > 0 && acc[ord[j - 1]] > acc[c]) { ord[j] = ord[j - 1]; j--; }
-            ord[j] = (uint8_t)c;
+            uint32_t rank = 0;
+#pragma unroll
+            for (int c2 = 0; c2 < KB; c2++)
+                if ((uint32_t)c2 < k && (acc[c2] < acc[c] || (acc[c2] == acc[c] && c2 < c))) rank++;
+            order[v * k + rank] = (uint8_t)c;
         }
     }
-    for (uint32_t c = 0; c < k; c++) order[v * k + c] = ord[c];
 }
 
 struct PartState {
@@ -305,8 +337,34 @@ __device__ uint64_t grid_round(const PartArgs& a, PartState* gs, GridScratch* g,
     const uint32_t k = a.k, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = GT / 32;
     const uint64_t lo = max(start, s0);
     uint32_t picks[KMAX];
+    // the choices of this thread's vectors are computed once per round (a segment is usually one
+    // vector) instead of once per cluster; longer segments / wide omega recompute them
+    constexpr uint32_t SEGC = 2, PMAX = 3;
+    const uint32_t nv = s1 > lo ? (uint32_t)(s1 - lo) : 0;
+    const bool cached = nv <= SEGC && (PRIM || a.omega - 1 <= PMAX);
+    uint32_t cch[SEGC][PMAX], cnp[SEGC] = {0, 0};
+    if (cached) {
+#pragma unroll
+        for (uint32_t t = 0; t < SEGC; t++) {
+            if (t >= nv) break;
+            if (PRIM) {
+                cch[t][0] = primary_choice(a, lo + t, open);
+                cnp[t] = 1;
+            } else {
+                cnp[t] = replica_picks(a, lo + t, open, tau, radius, picks);
+                for (uint32_t i = 0; i < PMAX; i++) cch[t][i] = i < cnp[t] ? picks[i] : 0xFFFFFFFFu;
+            }
+        }
+    }
     auto count_mine = [&](uint32_t c) -> uint32_t {
         uint32_t m = 0;
+        if (cached) {
+#pragma unroll
+            for (uint32_t t = 0; t < SEGC; t++)
+#pragma unroll
+                for (uint32_t i = 0; i < PMAX; i++) m += (i < cnp[t] && cch[t][i] == c) ? 1u : 0u;
+            return m;
+        }
         for (uint64_t v = lo; v < s1; v++) {
             if (PRIM) {
                 m += primary_choice(a, v, open) == c;
@@ -507,8 +565,32 @@ sg_status partition_run(const void* x, sg_dtype dtype, uint64_t n, uint32_t d, c
     const uint64_t cap = p->capacity ? p->capacity : derive_capacity(n, p->k, p->theta0_ppm);
     SG_CHECK_ARG(cap * p->k >= n, "partition: capacity * k < n");
     const uint64_t nwarps = (n + 31) / 32;
-    centroid_dist_order<<<(unsigned)((nwarps + 7) / 8), 256, 0, st>>>(x, dtype, n, d, C, p->k, dist, order);
-    SG_LAUNCHED("centroid_dist_order");
+    {
+        const unsigned g = (unsigned)((nwarps + 7) / 8);
+        const size_t cb = (size_t)p->k * d * sizeof(float);
+        const bool sm = cb <= 160 * 1024;   // + the 34 KB transpose tile, within the 227 KB budget
+        cudaError_t ae = cudaSuccess;
+        auto launch = [&](auto kern) {
+            if (sm) ae = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cb);
+            kern<<<g, 256, sm ? cb : 0, st>>>(x, dtype, n, d, C, p->k, dist, order);
+        };
+        const uint32_t k = p->k;
+        if (sm) {
+            if (k <= 4) launch(centroid_dist_order<4, true>);
+            else if (k <= 8) launch(centroid_dist_order<8, true>);
+            else if (k <= 16) launch(centroid_dist_order<16, true>);
+            else if (k <= 32) launch(centroid_dist_order<32, true>);
+            else launch(centroid_dist_order<64, true>);
+        } else {
+            if (k <= 4) launch(centroid_dist_order<4, false>);
+            else if (k <= 8) launch(centroid_dist_order<8, false>);
+            else if (k <= 16) launch(centroid_dist_order<16, false>);
+            else if (k <= 32) launch(centroid_dist_order<32, false>);
+            else launch(centroid_dist_order<64, false>);
+        }
+        SG_CUDA(ae);
+        SG_LAUNCHED("centroid_dist_order");
+    }
     PartArgs a{};
     a.dist = dist; a.order = order; a.home = home; a.primary_d = primary_d; a.state = state;
     a.n = n; a.cap = cap; a.k = p->k; a.omega = p->omega; a.block = p->block_size; a.theta0 = p->theta0_ppm;
