@@ -184,7 +184,7 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2605_10135_b200 import api, datagen
-    from paper_2605_10135_b200.pipeline import BuildConfig, build_index
+    from paper_2605_10135_b200.pipeline import BuildConfig, build_index, distribute_dataset, owned_rows
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -264,22 +264,25 @@ def main():
     # ---------------- e2e through the public API with host buffers
     e2e = None
     if not args.no_e2e:
-        xh = x.cpu().pin_memory()
+        # this rank's slice crosses PCIe, the rest arrives over NVLink (pipeline.distribute_dataset);
+        # the merged rows this rank owns are read back
+        rows = n // world
+        xh = x[rank * rows:(rank + 1) * rows].cpu().pin_memory()
         h2d = xh.numel() * xh.element_size()
-        d2h = 0
+        # the owned rows (same partition every step) and a pinned host buffer, set up before timing
+        own = None if world == 1 else owned_rows(idx, rank)
+        shape = tuple(idx.merged.shape) if own is None else (int(own.sum().item()), idx.merged.shape[1])
+        outh = torch.empty(shape, dtype=idx.merged.dtype, pin_memory=True)
+        d2h = outh.numel() * outh.element_size()
         barrier()
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        outh = None
         for _ in range(args.steps):
-            xd = xh.to("cuda", non_blocking=True)
+            xd = distribute_dataset(xh.to("cuda", non_blocking=True), n, rank, world)
             ix = step(xd)
-            if outh is None:   # pinned host buffer for the merged graph (allocated once, untimed cost)
-                outh = torch.empty(ix.merged.shape, dtype=ix.merged.dtype, pin_memory=True)
-            outh.copy_(ix.merged, non_blocking=True)
-            d2h = outh.numel() * outh.element_size()
+            outh.copy_(ix.merged if own is None else ix.merged[own], non_blocking=True)
         e1.record()
         torch.cuda.synchronize()
         barrier()

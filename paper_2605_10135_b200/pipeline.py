@@ -86,6 +86,18 @@ def exchange_records(sendbuf: torch.Tensor, send: list, recv: list, W: int) -> t
     return recvbuf
 
 
+def distribute_dataset(x_local: torch.Tensor, n: int, rank: int, world: int) -> torch.Tensor:
+    """Every rank holds the full dataset (the partition runs identically everywhere),
+    but only its contiguous 1/world slice crosses PCIe: the slices are all-gathered over NVLink.
+    `x_local` is this rank's rows [rank*n/world, (rank+1)*n/world) on the device."""
+    if world == 1:
+        return x_local
+    assert n % world == 0, "n must be a multiple of the world size"
+    full = torch.empty((n,) + tuple(x_local.shape[1:]), dtype=x_local.dtype, device=x_local.device)
+    dist.all_gather_into_tensor(full, x_local.contiguous())
+    return full
+
+
 class _Timer:
     def __init__(self, on: bool):
         self.on = on

@@ -133,3 +133,25 @@ def test_lpt_owner_properties():
             assert len({o[s] for s in range(4)}) == 4
         load = [sum(sizes[s] ** 2 for s in range(len(sizes)) if o[s] == r) for r in range(world)]
         assert max(load) <= max(sizes) ** 2 + min(l for l in load) or world == 1
+
+
+def _gather_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2605_10135_b200 import datagen, pipeline
+        x = datagen.sift_like(1000, 16, seed=3)
+        rows = 1000 // world
+        full = pipeline.distribute_dataset(x[rank * rows:(rank + 1) * rows].clone(), 1000, rank, world)
+        out[rank] = bool(torch.equal(full, x))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_distribute_dataset_world2():
+    """Each rank uploads only its slice; the all-gather rebuilds the full dataset everywhere."""
+    port = _free_port()
+    with mp.Manager() as mgr:
+        out = mgr.dict()
+        mp.spawn(_gather_worker, args=(2, port, out), nprocs=2, join=True)
+        assert dict(out) == {0: True, 1: True}
