@@ -61,10 +61,12 @@ __global__ void __launch_bounds__(RW * 32) reverse_merge_kernel(const uint32_t* 
                 const uint32_t keep = nrev;                       // sorted survivors at buf[0..keep)
                 const uint64_t rem = deg - done, room = SEGBUF - keep;
                 const uint64_t take = rem < room ? rem : room;
-                for (uint32_t i = lane; i < SEGBUF - keep; i += 32)
+                uint32_t np = 32;   // sort only the next power of two >= the entries present
+                while (np < keep + take) np <<= 1;
+                for (uint32_t i = lane; i < np - keep; i += 32)
                     buf[keep + i] = i < take ? keys[b0 + done + i] : ~0ull;
                 __syncwarp();
-                warp_sort_u64(buf, SEGBUF, lane);
+                warp_sort_u64(buf, np, lane);
                 done += take;
                 nrev = (uint32_t)((uint64_t)R < keep + take ? (uint64_t)R : keep + take);
             }
