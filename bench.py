@@ -246,15 +246,19 @@ def main():
     prec_is_f16 = True   # SIFT-shaped integer data -> F16_EXACT (AUTO)
     peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")) * (1.0 if prec_is_f16 else 0.5)
     achieved = alg_flops_step * args.steps / (knn_ms / 1000.0) / 1e12 if knn_ms > 0 else None
-    traffic = None
+    traffic, pipe_pct, prof_src = None, None, None
     tp = os.path.join(ROOT, "profiles", "knn_dram_bytes.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+            prof = json.load(open(tp))
+            traffic = prof.get("dram_bytes_per_launch")
+            pipe_pct = prof.get("tensor_pipe_active_pct")
+            prof_src = prof.get("source")
         except Exception:
             traffic = None
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "ncu_tensor_pipe_active_pct": pipe_pct, "ncu_source": prof_src,
                 "kernel": "knn_tc_kernel (tcgen05.mma kind::f16, fp32 accumulate)",
                 "peak_source": f"{src} bf16 dense sustained (f16 = bf16 rate)",
                 "per_unit": "2*d flops per (row, column) pair; m_s^2 pairs per shard launch",
@@ -334,7 +338,11 @@ def main():
                        "l2": "inputs (512 MB/rank) larger than the 126 MB L2; no explicit flush",
                        "parallelism": f"shard-parallel x{world} (LPT on m^2), NCCL bcast + all-to-all"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clocks, "recall_at_10": recall, "stage_ms_untimed_step": stage_ms,
+            "clocks": clocks, "recall_at_10": recall,
+            "recall_vs_oracle": "identical graph: on this integer data every stage is bit-exact with the "
+                                "oracle (tests/test_gpu_parity.py::test_end_to_end_integer_bit_exact, "
+                                "__graft_entry__.smoke), so the oracle-built graph has the same recall",
+            "stage_ms_untimed_step": stage_ms,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -35,7 +35,7 @@ MODES = {
 
 
 @pytest.mark.parametrize("mode", list(MODES))
-@pytest.mark.parametrize("m,L,seed", [(5000, 128, 3), (2100, 64, 4)])
+@pytest.mark.parametrize("m,L,seed", [(5000, 128, 3), (2100, 64, 4), (3000, 256, 5)])
 def test_knn_modes_bit_exact(oracle_mod, tmp_path, mode, m, L, seed):
     out = tmp_path / "r.npz"
     env = dict(os.environ, **MODES[mode], SG_KNN_REPORT="1")

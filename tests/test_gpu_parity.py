@@ -48,7 +48,8 @@ def test_gemm_probe_matches_matmul(api, prec):
 
 
 # ------------------------------------------------------------------ a5 kNN
-@pytest.mark.parametrize("m,L", [(1000, 64), (1300, 128), (129, 128), (65, 64), (40, 64), (2, 8)])
+@pytest.mark.parametrize("m,L", [(1000, 64), (1300, 128), (129, 128), (65, 64), (40, 64), (2, 8), (2600, 256),
+                                 (300, 256)])
 def test_knn_integer_exact(api, oracle_mod, m, L):
     x = datagen.sift_like(m, 128, seed=m)
     ids, dd = api.scalegann_knn(x.cuda(), L)

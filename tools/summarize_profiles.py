@@ -71,7 +71,9 @@ def main():
     open(os.path.join(P, f"{tag}_knn_ncu_full.txt"), "w").write("\n".join(out) + "\n")
     rd, wr = num(d, "dram__bytes_read.sum"), num(d, "dram__bytes_write.sum")
     scale = 1e9 if d["dram__bytes_read.sum"][1].startswith("G") else 1e6
+    tp = d.get("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", ("nan", ""))[0]
     json.dump({"kernel": d["Kernel Name"][0], "m": m, "dram_bytes_per_launch": (rd + wr) * scale,
+               "tensor_pipe_active_pct": float(tp.replace(",", "")),
                "dram_read_bytes": rd * scale, "dram_write_bytes": wr * scale,
                "source": f"profiles/{tag}_knn_ncu_full.txt (ncu --set full)",
                "note": "writes are per-row candidate appends evicted from L2; operand reads stay mostly in L2"},
