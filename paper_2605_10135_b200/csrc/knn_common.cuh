@@ -16,9 +16,6 @@ constexpr uint32_t BM = MSUB * NACC_MAX; // rows per CTA row block (operand padd
 #ifndef SG_BN
 #define SG_BN 128
 #endif
-#ifndef SG_ATM
-#define SG_ATM 0
-#endif
 #ifndef SG_KNN_PROF
 #define SG_KNN_PROF 0   // 1: per-warp cycle counters (diagnostics build only; costs registers + local memory)
 #endif
@@ -32,7 +29,6 @@ constexpr uint32_t NEPI = 8;             // epilogue warps
 constexpr uint32_t NTHREADS = 64 + NEPI * 32;
 constexpr uint32_t MAX_STAGES = 32;
 constexpr uint32_t NBUF_MAX = 4;         // TMEM buffers per accumulator: 4 (A in smem) or 2 (A in TMEM)
-constexpr uint32_t ACOL = 256;           // A in TMEM: half a at columns ACOL + 128 a
 constexpr uint32_t KSTRIDE = 36;         // floats per staged row (16B aligned, conflict-free)
 constexpr uint32_t SCRATCH = 32 * KSTRIDE * 4 + 64 * 4;   // per warp: staged keys | hist | sort buffer, + tile ids
 constexpr uint32_t SORT_MAX = 512;      // final sort buffer (u64 entries, aliases the staged keys)
@@ -103,19 +99,6 @@ __device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&v)[3
           "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
         : "r"(taddr));
 }
-__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
-                 "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
-                 : "memory");
-}
-__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-// tcgen05.mma with A from tensor memory (TS)
-__device__ __forceinline__ void tc_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(acc));
-}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // Shared-memory matrix descriptors, K-major: 128B swizzle (8-row groups 1024 B apart) and
@@ -181,7 +164,6 @@ struct KnnParams {
     int noepi;                 // diagnostics: epilogue only drains TMEM (pipeline speed test)
     int noload;                // diagnostics: producer skips the B loads (tensor-core speed test)
     int abl;                   // diagnostics ablation bits: 1 no insertion, 2 no id fetch, 4 no clock64
-    const uint4* a_glob;       // A side operand rows (for A-in-TMEM), kdim halves per row
     uint32_t a_words;          // 32-bit words per A row
 };
 

@@ -7,22 +7,25 @@
 // the tensor-core accumulator IS the key (exact in fp32 for integer data: every partial sum is
 // an integer below 2^24).  dist = |a_i|^2 + key is formed once per output.
 //
-// Pipeline (persistent, one CTA per SM, 10 warps).  A CTA owns a 256-row block held resident
-// in shared memory as two 128-row halves (NKA 128B-swizzle atoms + an optional 32B-swizzle
-// "mini" atom for the K tail each); every 64-column B tile streamed in is used by BOTH halves
-// (two M=128, N=64 MMAs), which halves the operand bytes per flop that L2 must deliver.
-//   warp 0: TMA producer (A block, then the B tiles through a ring of 8 KB slots; the column
-//           sweep of a row block starts t_back tiles before its diagonal when the shard is in
-//           spatial order, so the row's neighbourhood is seen first).
-//   warp 1: TMEM allocator + single-thread tcgen05.mma issuer, accumulators
-//           [half a][buffer b] = 64 TMEM columns each, 2 x 4 buffers = all 512 columns.
-//   warps 2..9: epilogue; warp (q, a) owns rows a*128 + q*32 + lane (TMEM lane quadrant q of
-//           accumulator a).  Per tile a thread (= one row) builds a 64-bit pass mask with FADD2
-//           + funnel shifts (sign of key - threshold, 1.5 instructions per element) and appends
-//           only set bits, as (key bits << 32 | id), to its row's candidate buffer (global, L2
-//           resident).  When a buffer nears full, the warp radix-selects (8-bit digits, smem
-//           histogram) a small superset of the L best and lowers the threshold; at the end of a
-//           row block the exact top-L is selected and sorted by (dist, id).
+// Pipeline (persistent, one CTA per SM, 18 warps).  A CTA owns a 256-row block (f16; 128 for
+// tf32) held resident in shared memory as 128-row halves (NKA 128B-swizzle atoms + an optional
+// 32B-swizzle "mini" atom for the K tail); every 128-column B tile streamed in is used by both
+// halves (two M=128, N=128 MMAs), which halves the operand bytes per flop that L2 must deliver.
+// Rows wider than 4 atoms use the streamed-A instantiation (NKA = 0): A and B atoms share the
+// ring slots and one 128-row accumulator.
+//   warp 0: TMA producer (A block, then the B tiles through a ring of 16 KB slots).
+//   warp 1: TMEM allocator + single-thread tcgen05.mma issuer; accumulators [half][buffer] of
+//           128 columns, 2 x 2 = all 512 columns, so a tile's MMAs overlap the previous drain.
+//   warps 2..17: epilogue in two column streams (columns [64 s, 64 s + 64) of every tile);
+//           warp (q, a, s) owns rows a*128 + q*32 + lane (TMEM lane quadrant q of half a).  Per
+//           32-column pass a thread (= one row) builds the pass mask with FADD2 + funnel shifts
+//           (sign of key - next_up(thr): 1.5 instructions per key) and appends only set bits, as
+//           (key bits << 32 | id), to its (row, stream) buffer (global, L2 resident).  A buffer
+//           that fills is compacted by ballot-count bit descent (select_pairs); the row threshold
+//           is one (key, id) pair in shared memory shared by both streams (atomicMin).  Thresholds
+//           are extrapolated from the fraction of columns seen (R15); the final phase checks each
+//           row (>= L union entries at or below the pair), selects and sorts its top-L, and lists
+//           the rows that fail for the fallback launch (rank-L thresholds).
 #include "knn_common.cuh"
 
 namespace sg {
@@ -49,9 +52,8 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     // f16 operands keep both 128-row halves of A resident; tf32 (wider A) keeps one
     constexpr uint32_t NACC = (KIND == 0 && !SA) ? NACC_MAX : 1;
     constexpr uint32_t RB = MSUB * NACC;                  // rows per row block of this instantiation
-    constexpr bool ATM = KIND == 0 && SG_ATM;
-    constexpr uint32_t NBUF = ATM ? 2 : 512 / (NACC * BN);
-    constexpr uint32_t AHALF = (ATM || SA) ? 0u : NKA * ATOM + (MINI ? MINIB : 0u);   // smem bytes of one resident half
+    constexpr uint32_t NBUF = 512 / (NACC * BN);
+    constexpr uint32_t AHALF = SA ? 0u : NKA * ATOM + (MINI ? MINIB : 0u);   // smem bytes of one resident half
     // offsets from smem_raw (not integer casts) so the compiler keeps shared-space accesses (LDS/STS)
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sA = smem;                                    // [NACC][NKA atoms + mini] (SS mode)
@@ -72,7 +74,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
 
     if (threadIdx.x == 0) {
         for (uint32_t s = 0; s < p.stages; s++) { mbar_init(&bars->full[s], 1); mbar_init(&bars->empty[s], 1); }
-        mbar_init(&bars->a_full, ATM ? 4 * NACC : 1);
+        mbar_init(&bars->a_full, 1);
         mbar_init(&bars->a_empty, 1);
         for (uint32_t b = 0; b < NBUF_MAX; b++) { mbar_init(&bars->tm_full[b], 1); mbar_init(&bars->tm_empty[b], 8 * NACC); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -101,11 +103,11 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         if (lane == 0) {
             uint32_t stage = 0, sph = 0, it = 0;
             for (uint32_t rb = blockIdx.x; rb < n_rb; rb += gridDim.x, it++) {
-                if (!ATM && !SA) {
+                if (!SA) {
                     if (it > 0) mbar_wait(&bars->a_empty, (it - 1) & 1);
                     mbar_expect_tx(&bars->a_full, NACC * AHALF);
                 }
-                for (uint32_t a = 0; a < NACC && !ATM && !SA; a++) {
+                for (uint32_t a = 0; a < NACC && !SA; a++) {
                     uint8_t* base = sA + a * AHALF;
                     for (int ka = 0; ka < NKA; ka++)
                         tma_load_2d(&tmA, &bars->a_full, base + ka * ATOM, ka * ATOM_K, rb * RB + a * MSUB);
@@ -160,17 +162,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                         for (uint32_t a = 0; a < NACC; a++) {
                             const uint32_t dcol = tmem + (a * NBUF + buf) * BN;
                             const uint32_t abase = a_base + a * AHALF;
-                            if constexpr (ATM) {
-                                const uint32_t at = tmem + ACOL + a * 128;   // 8 columns per K step of 16
-                                if (ka < NKA) {
-#pragma unroll
-                                    for (uint32_t kk = 0; kk < 4; kk++)
-                                        tc_mma_ts(dcol, at + (ka * 4 + kk) * 8, desc_sw128(bslot + kk * 32), idesc,
-                                                  (ka | kk) != 0);
-                                } else {
-                                    tc_mma_ts(dcol, at + NKA * 32, desc_sw32(bslot), idesc, NKA != 0);
-                                }
-                            } else if constexpr (SA) {
+                            if constexpr (SA) {
                                 const uint32_t aslot = bslot + SLOT;   // this K atom of A
                                 if (ka < nka) {
 #pragma unroll
@@ -196,7 +188,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     }
                     tc_commit(&bars->tm_full[buf]);
                 }
-                if (!ATM && !SA) tc_commit(&bars->a_empty);
+                if (!SA) tc_commit(&bars->a_empty);
             }
         }
     } else {
@@ -428,7 +420,7 @@ uint32_t keep_target(uint32_t L, uint32_t C) {
 template <int KIND, int NKA, int MINI, int EPL>
 sg_status launch_t(const CUtensorMap* maps, KnnParams& p, cudaStream_t st) {
     constexpr bool SA = NKA == 0;
-    constexpr uint32_t AHALF = ((KIND == 0 && SG_ATM) || SA) ? 0u : NKA * ATOM + (MINI ? MINIB : 0u);
+    constexpr uint32_t AHALF = SA ? 0u : NKA * ATOM + (MINI ? MINIB : 0u);
     constexpr uint32_t NACC = (KIND == 0 && !SA) ? NACC_MAX : 1;
     constexpr uint32_t SLOTB = SA ? 2 * SLOT : SLOT;
     const size_t fixed = NACC * AHALF + sizeof(Bars) + 128 + BM * 8 + 2 * BM * 4 + 8 * NACC * SCRATCH + 1024 + 64;
@@ -552,7 +544,6 @@ sg_status knn_core(const Operand& A, const Operand& B, int /*metric*/, bool self
     if (A.rows_pad % BM || B.rows_pad % BN) { set_error("kNN: operand rows not padded"); return SG_ERR_INVALID_ARG; }
     KnnParams p{};
     p.norm_a = A.norm;
-    p.a_glob = (const uint4*)A.a;
     p.a_words = A.kdim * A.esize / 4;
     p.C = cand_cap(L);
     p.keep_max = keep_target(L, p.C);
@@ -614,7 +605,6 @@ sg_status knn_core(const Operand& A, const Operand& B, int /*metric*/, bool self
     p2.alpha100 = 0;
     if (tr) p2.C = knn_t_cap(L, false);
     p2.norm_a = A2.norm;
-    p2.a_glob = (const uint4*)A2.a;
     p2.n_rows_dev = fail_count;
     p2.row_map = fail_rows;
     p2.self_col = self_exclude ? fail_rows : nullptr;
