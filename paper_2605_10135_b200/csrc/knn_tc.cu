@@ -35,7 +35,9 @@ namespace {
 constexpr uint32_t NEPI_R = 16;                         // epilogue warps (2 column streams x 8)
 constexpr uint32_t NTHREADS_R = 64 + NEPI_R * 32;
 
-template <int KIND, int NKA, int MINI, int EPL>
+// DIAG: the instantiation that honours the probe / diagnostics switches (raw accumulator dump,
+// stubbed epilogue, ablations); production launches use DIAG = false and skip those tests.
+template <int KIND, int NKA, int MINI, int EPL, bool DIAG>
 __global__ void __launch_bounds__(NTHREADS_R, 1)
 knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmAm, const __grid_constant__ CUtensorMap tmBm, KnnParams p) {
@@ -119,7 +121,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     for (uint32_t ka = 0; ka < nslot; ka++) {
                         mbar_wait(&bars->empty[stage], sph ^ 1);
                         uint8_t* slot = sB + stage * SLOTB;
-                        if (p.noload) {
+                        if (DIAG && p.noload) {
                             mbar_arrive(&bars->full[stage]);
                         } else if (ka < nka) {
                             mbar_expect_tx(&bars->full[stage], SA ? BATOM + ATOM : BATOM);
@@ -262,11 +264,11 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     c0 = clk();
                     pw[1] += c0 - c1;
                     const uint32_t col0 = t * BN + hp * 32;
-                    if (p.noepi) {
+                    if (DIAG && p.noepi) {
                         if ((v[0] ^ v[31]) == 0x7fc00001u) p.out_ids[0] = v[1];   // keep the loads live
                         continue;
                     }
-                    if (p.probe) {
+                    if (DIAG && p.probe) {
                         if (valid) {
 #pragma unroll
                             for (int j = 0; j < 32; j++)
@@ -291,7 +293,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     if (self_tile && scol - col0 < 32u) m &= ~(1u << (scol - col0));   // self column
                     c1 = clk();
                     pw[3] += c1 - c0;
-                    if (p.abl & 1) m = 0;
+                    if (DIAG && (p.abl & 1)) m = 0;
                     if (__any_sync(0xffffffffu, m != 0)) {
                         sids[lane] = p.col_map ? __ldg(p.col_map + col0 + lane) : col0 + lane;
                         float4* st4 = (float4*)(skeys + lane * KSTRIDE);
@@ -347,7 +349,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     pw[2] += c1 - c0;
                 }
             }
-            if (p.probe || p.noepi) continue;
+            if (DIAG && (p.probe || p.noepi)) continue;
             const long long f0 = clk();
             s_cnt[s][r] = cnt;
             named_bar_sync(1, nbar);
@@ -431,7 +433,15 @@ sg_status launch_t(const CUtensorMap* maps, KnnParams& p, cudaStream_t st) {
     if (stages > MAX_STAGES) stages = MAX_STAGES;
     p.stages = stages;
     const size_t smem = fixed + stages * SLOTB;
-    auto kern = knn_tc_kernel<KIND, NKA, MINI, EPL>;
+    // the diagnostics / probe instantiation exists for EPL = 8 only (the probe runs with L = 1 and
+    // the diagnostics with L <= 128), which keeps the number of kernels and the build time down
+    auto kern = knn_tc_kernel<KIND, NKA, MINI, EPL, false>;
+    if constexpr (EPL == 8) {
+        if (p.probe || p.noepi || p.noload || p.abl) kern = knn_tc_kernel<KIND, NKA, MINI, EPL, true>;
+    } else if (p.probe) {
+        set_error("kNN probe: unsupported candidate capacity");
+        return SG_ERR_UNSUPPORTED;
+    }
     SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const uint32_t grid = p.n_rb < (uint32_t)num_sms() ? p.n_rb : (uint32_t)num_sms();
     knn_time_begin(st);
