@@ -155,6 +155,21 @@ def test_partition_bit_exact(api, oracle_mod, block, kind):
     assert counts["sizes"] == r["sizes"].tolist() and counts["repl"] == r["repl"].tolist()
 
 
+@pytest.mark.parametrize("eps", [1.0, 1.05, 1.1, 1.5, 3.0])
+def test_partition_epsilon_sweep_bit_exact(api, oracle_mod, eps):
+    """§8(f) NEXT-2: the eps values of the paper's selectivity sweep, GPU == oracle,
+    and eps <= 1 places no replica (d' < eps * d is impossible for d' >= d)."""
+    n, k = 10_000, 8
+    x = datagen.sift_like(n, 128, seed=7)
+    C = x[:: n // k][:k].clone().contiguous()
+    home, pd, counts = api.scalegann_partition(x.cuda(), C.cuda(), omega=2, epsilon=eps, block_size=1024)
+    r = oracle_mod.partition(x.numpy(), C.numpy(), omega=2, eps=eps, block_size=1024)
+    assert np.array_equal(u32(home), r["home"])
+    assert counts["repl"] == r["repl"].tolist()
+    if eps <= 1.0:
+        assert sum(counts["repl"]) == 0
+
+
 def test_partition_capacity_binding_and_omega3(api, oracle_mod):
     x = _clustered(6000, 16, seed=9)
     C = x[:6].clone()                      # poor centroids -> capacity binds
@@ -264,18 +279,23 @@ def test_kmeans_distortion_within_1pct(api, oracle_mod):
 
 
 # ------------------------------------------------------------------ end to end (C0-sized)
-def test_end_to_end_integer_bit_exact(api, oracle_mod):
+@pytest.mark.parametrize("k,omega,eps", [(2, 2, 1.2), (3, 1, 1.0), (3, 2, 3.0)])
+def test_end_to_end_integer_bit_exact(api, oracle_mod, k, omega, eps):
     """SIFT-shaped integer data: every stage is exact, so the GPU merged graph equals the
-    oracle-built graph bit for bit (same centroids fed to both)."""
+    oracle-built graph bit for bit (same centroids fed to both).  (3, 1, 1.0) is the split-only
+    build of P:432-470 (no replicas); (3, 2, 3.0) the most selective-replication-heavy end of
+    the eps sweep (§8(f) NEXT-2)."""
     from paper_2605_10135_b200.pipeline import BuildConfig, build_index
     x = datagen.sift_like(6000, 128, seed=61)
-    cfg = BuildConfig(k=2, L=64, R=32, block_size=1024)
+    cfg = BuildConfig(k=k, omega=omega, epsilon=eps, L=64, R=32, block_size=1024)
     idx = build_index(x.cuda(), cfg)
     C = idx.centroids.cpu().numpy()
-    r = oracle_mod.partition(x.numpy(), C, omega=2, block_size=1024)
+    r = oracle_mod.partition(x.numpy(), C, omega=omega, eps=eps, block_size=1024)
     assert np.array_equal(u32(idx.home), r["home"])
+    if omega == 1:
+        assert int(r["repl"].sum()) == 0
     idm, gs, gds = [], [], []
-    for s in range(2):
+    for s in range(k):
         im = oracle_mod.idmap(r["home"], s)
         ids, dd = oracle_mod.knn(x.numpy(), 64, ida=im)
         pr, prd = oracle_mod.prune(ids, dd, 32)
