@@ -173,11 +173,25 @@ def run_reference(args):
             "impl": "reference",
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores(), "kind": "oracle", "sample": desc},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
+
+
+_OUT_FD = None
+
+
+def emit(line: dict):
+    """The one JSON line on the real stdout; everything else (NCCL's version banner, native
+    prints) was redirected to stderr by main()."""
+    fd = _OUT_FD if _OUT_FD is not None else 1
+    os.write(fd, (json.dumps(line) + "\n").encode())
 
 
 def main():
+    global _OUT_FD
     args = parse()
+    sys.stdout.flush()
+    _OUT_FD = os.dup(1)
+    os.dup2(2, 1)
     if args.impl == "reference":
         run_reference(args)
         return
@@ -344,7 +358,7 @@ def main():
                                 "__graft_entry__.smoke), so the oracle-built graph has the same recall",
             "stage_ms_untimed_step": stage_ms,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
