@@ -231,6 +231,24 @@ sg_status scalegann_search_eval(const void* x, sg_dtype dtype, uint64_t n, uint3
                                 const uint32_t* gt, uint32_t* gt_out, uint32_t* out_ids,
                                 double* recall_host, void* ws, size_t ws_bytes, void* stream);
 
+/* ---- a9, split-only mode: per-shard search + result merge (§8(f) NEXT-2;
+ * reading R15) ------------------------------------------------------------------
+ * The same beam search as scalegann_search_eval, run once from each of the n_entries entry
+ * points (entries_host, host, e.g. every shard's entry from scalegann_entry_points), each
+ * keeping its own beam; the per-entry top-topk lists are merged into the topk smallest
+ * distinct (dist, id).  For a split-only graph (omega = 1, disjoint shards) this is "search
+ * every shard and merge the results".  Errors as scalegann_search_eval, plus
+ * SG_ERR_INVALID_ARG for n_entries outside [1, 1024] or an entry >= n.  Synchronises when
+ * recall_host is not NULL. */
+sg_status scalegann_search_shards_workspace(uint64_t n, uint32_t d, sg_dtype dtype, uint32_t nq, uint32_t topk,
+                                            uint32_t beam, uint32_t n_entries, size_t* bytes);
+sg_status scalegann_search_eval_shards(const void* x, sg_dtype dtype, uint64_t n, uint32_t d,
+                                       const uint32_t* graph, uint32_t R, const uint32_t* entries_host,
+                                       uint32_t n_entries, const void* queries, uint32_t nq, uint32_t topk,
+                                       uint32_t beam, int32_t metric, const uint32_t* gt, uint32_t* gt_out,
+                                       uint32_t* out_ids, double* recall_host, void* ws, size_t ws_bytes,
+                                       void* stream);
+
 /* ---- diagnostics ------------------------------------------------------------
  * Raw distance-tile probe of the tcgen05 GEMM core (validation of the MMA
  * pipeline against a reference matmul): out[i][j] = a_i . b_j in fp32 for

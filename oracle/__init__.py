@@ -220,6 +220,24 @@ def search(x, graph, entry, queries, topk=10, beam=64, metric=0):
     return ids, dd, nd
 
 
+def search_shards(x, graph, entries, queries, topk=10, beam=64, metric=0):
+    """Split-only search (split-only systems search every shard and merge the
+    results; reading R15): P8 from each entry point with its own beam, then per query the
+    union of the per-entry top-topk lists ordered by (dist, id), each id once, first topk."""
+    per = [search(x, graph, e, queries, topk, beam, metric)[:2] for e in entries]
+    nq = per[0][0].shape[0]
+    out = np.full((nq, topk), SENT, np.uint32)
+    for qi in range(nq):
+        cand = {}
+        for ids, dd in per:
+            for i, dv in zip(ids[qi].tolist(), dd[qi].tolist()):
+                if i != SENT:
+                    cand[i] = dv
+        best = sorted(cand.items(), key=lambda t: (t[1], t[0]))[:topk]
+        out[qi, :len(best)] = [i for i, _ in best]
+    return out
+
+
 def recall(ret, gt, k=10):
     """recall@k = |ret[:, :k] & gt[:, :k]| / k averaged over queries."""
     ret = np.asarray(ret)[:, :k]

@@ -47,7 +47,7 @@ EXPORTS = [
     "scalegann_prune", "scalegann_reverse_workspace", "scalegann_reverse", "scalegann_build_shard_workspace",
     "scalegann_build_shard", "scalegann_optimize_from_knn", "scalegann_merge_counts", "scalegann_merge_workspace",
     "scalegann_merge_pack", "scalegann_merge_union", "scalegann_merge", "scalegann_search_workspace",
-    "scalegann_search_eval", "scalegann_gemm_probe", "scalegann_stats_enable", "scalegann_stats_read", "scalegann_knn_profile",
+    "scalegann_search_eval", "scalegann_search_shards_workspace", "scalegann_search_eval_shards", "scalegann_gemm_probe", "scalegann_stats_enable", "scalegann_stats_read", "scalegann_knn_profile",
 ]
 
 
@@ -100,6 +100,9 @@ def load(build_if_missing: bool = True):
         "scalegann_search_workspace": ([u64, u32, i32, u32, u32, u32, psz], i32),
         "scalegann_search_eval": ([vp, i32, u64, u32, vp, u32, u32, vp, u32, u32, u32, i32, vp, vp, vp,
                                    P(ctypes.c_double), vp, sz, vp], i32),
+        "scalegann_search_shards_workspace": ([u64, u32, i32, u32, u32, u32, u32, psz], i32),
+        "scalegann_search_eval_shards": ([vp, i32, u64, u32, vp, u32, P(u32), u32, vp, u32, u32, u32, i32, vp, vp,
+                                          vp, P(ctypes.c_double), vp, sz, vp], i32),
         "scalegann_gemm_probe": ([vp, u64, vp, u64, i32, u32, i32, vp, vp, sz, vp], i32),
         "scalegann_stats_enable": ([ctypes.c_int], i32),
         "scalegann_knn_profile": ([vp], i32),
@@ -430,4 +433,26 @@ def scalegann_search_eval(x, graph, entry, queries, topk=10, beam=64, metric=SG_
     _check(L.scalegann_search_eval(_ptr(x), _dtype(x), n, d, _ptr(graph), R, entry, _ptr(queries), nq, topk, beam,
                                    metric, _ptr(gt), _ptr(gt_out), _ptr(out), ctypes.byref(rec), p, nbytes,
                                    _stream()))
+    return out, (gt if gt is not None else gt_out), rec.value
+
+
+def scalegann_search_eval_shards(x, graph, entries, queries, topk=10, beam=64, metric=SG_L2, gt=None, ws=None):
+    """Split-only search: one beam per entry point, per-entry results merged.
+    Returns (out_ids nq x topk, gt nq x topk, recall)."""
+    L = load()
+    n, d = x.shape
+    R = graph.shape[1]
+    nq = queries.shape[0]
+    ne = len(entries)
+    ent = (ctypes.c_uint32 * ne)(*entries)
+    out = torch.empty(nq, topk, dtype=torch.int32, device=x.device)
+    gt_out = None
+    if gt is None:
+        gt_out = torch.empty(nq, topk, dtype=torch.int32, device=x.device)
+    rec = ctypes.c_double(0.0)
+    nb = _size_q(L.scalegann_search_shards_workspace, n, d, _dtype(x), nq, topk, beam, ne)
+    p, nbytes = _ws(nb, ws)
+    _check(L.scalegann_search_eval_shards(_ptr(x), _dtype(x), n, d, _ptr(graph), R, ent, ne, _ptr(queries), nq, topk,
+                                          beam, metric, _ptr(gt), _ptr(gt_out), _ptr(out), ctypes.byref(rec), p,
+                                          nbytes, _stream()))
     return out, (gt if gt is not None else gt_out), rec.value

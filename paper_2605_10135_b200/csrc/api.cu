@@ -39,7 +39,10 @@ sg_status merge_union_run(const uint32_t* home, const uint32_t* inv, uint64_t n,
 size_t beam_ws(uint64_t n, uint32_t nq);
 sg_status beam_run(const void* x, sg_dtype dtype, uint64_t n, uint32_t d, const uint32_t* graph, uint32_t R,
                    uint32_t entry, const void* q, uint32_t nq, uint32_t topk, uint32_t beam, int metric,
-                   uint32_t* out_ids, unsigned long long* ndist, Carver& cv, cudaStream_t st);
+                   uint32_t* out_ids, unsigned long long* ndist, Carver& cv, cudaStream_t st,
+                   uint64_t* out_keys = nullptr);
+sg_status shard_merge_run(const uint64_t* keys, uint32_t ns, uint32_t nq, uint32_t topk, uint32_t* out_ids,
+                          cudaStream_t st);
 sg_status recall_run(const uint32_t* ret, const uint32_t* gt, uint32_t nq, uint32_t topk, double* recall_host,
                      Carver& cv, cudaStream_t st);
 
@@ -449,6 +452,48 @@ sg_status scalegann_search_eval(const void* x, sg_dtype dtype, uint64_t n, uint3
         g = gbuf;
     }
     SG_TRY(beam_run(x, dtype, n, d, graph, R, entry, queries, nq, topk, beam, metric, out_ids, nullptr, cv, st));
+    if (recall_host) return recall_run(out_ids, g, nq, topk, recall_host, cv, st);
+    return SG_OK;
+}
+
+sg_status scalegann_search_shards_workspace(uint64_t n, uint32_t d, sg_dtype dtype, uint32_t nq, uint32_t topk,
+                                            uint32_t beam, uint32_t n_entries, size_t* bytes) {
+    SG_TRY(scalegann_search_workspace(n, d, dtype, nq, topk, beam, bytes));
+    *bytes += (size_t)n_entries * nq * topk * 8 + 512;
+    return SG_OK;
+}
+
+sg_status scalegann_search_eval_shards(const void* x, sg_dtype dtype, uint64_t n, uint32_t d, const uint32_t* graph,
+                                       uint32_t R, const uint32_t* entries_host, uint32_t n_entries,
+                                       const void* queries, uint32_t nq, uint32_t topk, uint32_t beam,
+                                       int32_t metric, const uint32_t* gt, uint32_t* gt_out, uint32_t* out_ids,
+                                       double* recall_host, void* ws, size_t ws_bytes, void* stream) {
+    SG_CHECK_ARG(x && graph && queries && out_ids && entries_host && nq > 0 && n > 0 && d > 0 && d <= 1024,
+                 "search_shards: bad arguments");
+    SG_CHECK_ARG(n_entries >= 1 && n_entries <= 1024, "search_shards: need 1 <= n_entries <= 1024");
+    for (uint32_t s = 0; s < n_entries; s++) SG_CHECK_ARG(entries_host[s] < n, "search_shards: entry out of range");
+    SG_CHECK_ARG(R >= 1 && R <= 128 && topk >= 1 && topk <= beam && beam <= 512, "search: need R<=128, topk<=beam<=512");
+    SG_CHECK_ARG(metric == SG_L2 || metric == SG_IP, "search: bad metric");
+    cudaStream_t st = S(stream);
+    Carver cv(ws, ws_bytes);
+    uint64_t* keys = cv.take<uint64_t>((size_t)n_entries * nq * topk);
+    if (!cv.ok()) { set_error("search_shards: workspace too small"); return SG_ERR_WORKSPACE; }
+    const uint32_t* g = gt;
+    if (!g) {
+        uint32_t* gbuf = gt_out ? gt_out : cv.take<uint32_t>((size_t)nq * topk);
+        float* gd = cv.take<float>((size_t)nq * topk);
+        if (!cv.ok()) { set_error("search_shards: workspace too small"); return SG_ERR_WORKSPACE; }
+        Carver kc = cv;
+        SG_TRY(knn_impl(queries, nullptr, nq, x, nullptr, n, dtype, d, 0, topk, metric, SG_PREC_AUTO, gbuf, gd, nullptr,
+                        kc.base ? kc.base + kc.off : nullptr, kc.cap > kc.off ? kc.cap - kc.off : 0, st));
+        g = gbuf;
+    }
+    for (uint32_t s = 0; s < n_entries; s++) {
+        Carver bc = cv;   // every per-entry search reuses the same visited-bitmap scratch
+        SG_TRY(beam_run(x, dtype, n, d, graph, R, entries_host[s], queries, nq, topk, beam, metric, nullptr, nullptr,
+                        bc, st, keys + (size_t)s * nq * topk));
+    }
+    SG_TRY(shard_merge_run(keys, n_entries, nq, topk, out_ids, st));
     if (recall_host) return recall_run(out_ids, g, nq, topk, recall_host, cv, st);
     return SG_OK;
 }

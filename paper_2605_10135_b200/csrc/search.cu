@@ -20,7 +20,8 @@ struct SearchArgs {
     const void* q;
     const uint32_t* graph;
     uint32_t* visited;     // batch x words
-    uint32_t* out_ids;
+    uint32_t* out_ids;     // may be NULL when out_keys is set
+    uint64_t* out_keys;    // optional: the first topk pool keys (ord(dist) << 32 | id), ~0 past np
     uint64_t n, words;
     uint32_t d, R, entry, nq, q0, topk, beam, poolcap, newcap;
     int dtype, metric;
@@ -133,8 +134,10 @@ __global__ void __launch_bounds__(SW * 32) beam_kernel(SearchArgs a) {
         for (uint32_t i = lane; i < np; i += 32) { pool[i] = pool2[i]; ex[i] = ex2[i]; }
         __syncwarp();
     }
-    for (uint32_t i = lane; i < a.topk; i += 32)
-        a.out_ids[(uint64_t)qi * a.topk + i] = i < np ? (uint32_t)pool[i] : SG_SENT;
+    for (uint32_t i = lane; i < a.topk; i += 32) {
+        if (a.out_ids) a.out_ids[(uint64_t)qi * a.topk + i] = i < np ? (uint32_t)pool[i] : SG_SENT;
+        if (a.out_keys) a.out_keys[(uint64_t)qi * a.topk + i] = i < np ? pool[i] : ~0ull;
+    }
     if (lane == 0 && a.ndist) atomicAdd(a.ndist, nd);
 }
 
@@ -151,6 +154,30 @@ __global__ void recall_kernel(const uint32_t* __restrict__ ret, const uint32_t* 
     atomicAdd(hits, h);
 }
 
+// Per-shard search + result merge (split-only mode; reading R15): keys[s][q][0..topk)
+// are the per-entry results; the merged list is the topk smallest distinct keys, i.e. the union
+// ordered by (dist, id) with duplicate ids (the same vector reached from two entries) kept once.
+__global__ void shard_merge_kernel(const uint64_t* __restrict__ keys, uint32_t ns, uint32_t nq, uint32_t topk,
+                                   uint32_t* __restrict__ out) {
+    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    uint64_t last = 0;
+    bool first = true;
+    for (uint32_t i = 0; i < topk; i++) {
+        uint64_t best = ~0ull;
+        for (uint32_t s = 0; s < ns; s++) {
+            const uint64_t* row = keys + ((uint64_t)s * nq + q) * topk;
+            for (uint32_t j = 0; j < topk; j++) {
+                const uint64_t k = row[j];
+                if ((first || k > last) && k < best) best = k;
+            }
+        }
+        out[(uint64_t)q * topk + i] = best == ~0ull ? SG_SENT : (uint32_t)best;
+        last = best;
+        first = false;
+    }
+}
+
 }  // namespace
 
 static uint32_t pow2_at_least(uint32_t v) { uint32_t p = 32; while (p < v) p <<= 1; return p; }
@@ -165,7 +192,8 @@ size_t beam_ws(uint64_t n, uint32_t nq) {
 
 sg_status beam_run(const void* x, sg_dtype dtype, uint64_t n, uint32_t d, const uint32_t* graph, uint32_t R,
                    uint32_t entry, const void* q, uint32_t nq, uint32_t topk, uint32_t beam, int metric,
-                   uint32_t* out_ids, unsigned long long* ndist, Carver& cv, cudaStream_t st) {
+                   uint32_t* out_ids, unsigned long long* ndist, Carver& cv, cudaStream_t st,
+                   uint64_t* out_keys) {
     const uint64_t words = (n + 31) / 32;
     uint64_t batch = (1ull << 30) / (words * 4 + 1);
     if (batch < SW) batch = SW;
@@ -174,7 +202,7 @@ sg_status beam_run(const void* x, sg_dtype dtype, uint64_t n, uint32_t d, const 
     uint32_t* vis = cv.take<uint32_t>(batch * words);
     if (!cv.ok()) { set_error("search: workspace too small"); return SG_ERR_WORKSPACE; }
     SearchArgs a{};
-    a.x = x; a.q = q; a.graph = graph; a.visited = vis; a.out_ids = out_ids; a.n = n; a.words = words;
+    a.x = x; a.q = q; a.graph = graph; a.visited = vis; a.out_ids = out_ids; a.out_keys = out_keys; a.n = n; a.words = words;
     a.d = d; a.R = R; a.entry = entry; a.nq = nq; a.topk = topk; a.beam = beam;
     a.poolcap = pow2_at_least(beam + R);
     a.newcap = pow2_at_least(R);
@@ -189,6 +217,13 @@ sg_status beam_run(const void* x, sg_dtype dtype, uint64_t n, uint32_t d, const 
         beam_kernel<<<(unsigned)((cnt + SW - 1) / SW), SW * 32, smem, st>>>(a);
         SG_LAUNCHED("beam_kernel");
     }
+    return SG_OK;
+}
+
+sg_status shard_merge_run(const uint64_t* keys, uint32_t ns, uint32_t nq, uint32_t topk, uint32_t* out_ids,
+                          cudaStream_t st) {
+    shard_merge_kernel<<<(nq + 127) / 128, 128, 0, st>>>(keys, ns, nq, topk, out_ids);
+    SG_LAUNCHED("shard_merge_kernel");
     return SG_OK;
 }
 

@@ -270,6 +270,24 @@ def test_search_matches_oracle(api, oracle_mod):
     assert abs(rec - oracle_mod.recall(oo, ogt)) < 1e-12
 
 
+def test_search_shards_split_only_matches_oracle(api, oracle_mod):
+    """Split-only build (k = 3, omega = 1) searched per shard with result merge (P:432-470,
+    reading R15): GPU == oracle list for list; per-shard search beats one global beam."""
+    from paper_2605_10135_b200.pipeline import BuildConfig, build_index
+    x = datagen.sift_like(6000, 64, seed=43)
+    idx = build_index(x.cuda(), BuildConfig(k=3, omega=1, epsilon=1.0, L=32, R=16, block_size=1024))
+    _, entries = api.scalegann_entry_points(idx.home, idx.primary_d, idx.sizes)
+    q = datagen.sift_like(200, 64, seed=44)
+    out, gt, rec = api.scalegann_search_eval_shards(x.cuda(), idx.merged, entries, q.cuda(), topk=10, beam=32)
+    oo = oracle_mod.search_shards(x.numpy(), u32(idx.merged), entries, q.numpy(), topk=10, beam=32)
+    assert np.array_equal(u32(out), oo)
+    ogt, _ = oracle_mod.knn(q.numpy(), 10, xb=x.numpy(), self_exclude=False)
+    assert np.array_equal(u32(gt), ogt)
+    assert abs(rec - oracle_mod.recall(oo, ogt)) < 1e-12
+    _, _, rec1 = api.scalegann_search_eval(x.cuda(), idx.merged, idx.entry, q.cuda(), topk=10, beam=32, gt=gt)
+    assert rec > rec1
+
+
 # ------------------------------------------------------------------ a1 k-means
 def test_kmeans_distortion_within_1pct(api, oracle_mod):
     x = datagen.sift_like(50_000, 128, seed=51)

@@ -345,6 +345,26 @@ def test_search_full_beam_is_exact(oracle_mod):
     assert oracle_mod.recall(gt, gt) == 1.0
 
 
+def test_search_shards_disconnected_full_beam_is_exact(oracle_mod):
+    # Split-only graph: two disjoint shards, each a ring-connected kNN graph of its
+    # own members.  One beam from a single entry cannot leave its shard; one full beam per
+    # shard entry + the merge of the results must give the exact top-k over all points.
+    rng = np.random.default_rng(18)
+    X = rng.normal(size=(160, 5)).astype(np.float32)
+    parts = [np.arange(0, 160, 2), np.arange(1, 160, 2)]
+    graph = np.full((160, 9), 0xFFFFFFFF, np.uint32)
+    for ids_s in parts:
+        loc, _ = oracle_mod.knn(X[ids_s], 8)
+        graph[ids_s, :8] = ids_s[loc]
+        graph[ids_s, 8] = np.roll(ids_s, -1)
+    Q = rng.normal(size=(15, 5)).astype(np.float32)
+    gt, _ = oracle_mod.knn(Q, 10, xb=X, self_exclude=False)
+    res = oracle_mod.search_shards(X, graph, [0, 1], Q, topk=10, beam=80)
+    assert np.array_equal(res, gt)
+    one, _, nd = oracle_mod.search(X, graph, 0, Q, topk=10, beam=80)
+    assert (one % 2 == 0).all() and (nd == 80).all()          # a single beam stays in shard 0
+
+
 def test_search_query_is_data_point(oracle_mod):
     rng = np.random.default_rng(16)
     X = rng.normal(size=(100, 3)).astype(np.float32)

@@ -10,8 +10,9 @@ warm-up call first.
 NEXT-2 — selectivity sweep (Table 4 / Fig. 3): eps in {1.0, 1.1, 1.2, 1.5, 3.0} with
 omega = 2, plus the split-only build (omega = 1, no replicas): replication proportion
 (replicas / n), device build time per step, recall@10 at beam 64.  The split-only graph is
-searched from the single global entry point like the others; the paper's split-only systems
-(GGNN / Extended CAGRA) search every shard and merge results instead, which is not built here.
+searched both from the single global entry point and per shard with result merge
+(`scalegann_search_eval_shards`, one beam of 64 per shard entry), as the paper's split-only
+systems (GGNN / Extended CAGRA) search.
 
     python tools/sweep_next.py [--n 1000000] > gpurun_out/sweep_next.json
 """
@@ -65,10 +66,13 @@ def main():
             _, gt, _ = api.scalegann_search_eval(x, idx.merged, idx.entry, q, topk=10, beam=64)
         _, _, rec = api.scalegann_search_eval(x, idx.merged, idx.entry, q, topk=10, beam=64, gt=gt)
         repl = sum(idx.counts["repl"])
+        _, entries = api.scalegann_entry_points(idx.home, idx.primary_d, idx.sizes)
+        _, _, rec_sh = api.scalegann_search_eval_shards(x, idx.merged, entries, q, topk=10, beam=64, gt=gt)
         out["next2_selectivity"].append({"omega": omega, "epsilon": eps, "replicas": repl,
                                          "replication_proportion": repl / n, "shard_sizes": idx.sizes,
                                          "build_ms": ms, "build_vectors_per_s": n / (ms / 1000.0),
-                                         "recall_at_10_beam64": rec})
+                                         "recall_at_10_beam64": rec,
+                                         "recall_at_10_beam64_per_shard_search": rec_sh})
         if omega == 2 and eps == 1.2:
             base = idx
         del idx
