@@ -36,6 +36,20 @@ __device__ __forceinline__ float qdist(const SearchArgs& a, const float* qv, uin
             const float t = (float)row[j];
             s = a.metric == SG_IP ? __fmaf_rn(-t, qv[j], s) : __fmaf_rn(t - qv[j], t - qv[j], s);
         }
+    } else if ((a.d & 3) == 0 && ((uintptr_t)a.x & 15) == 0) {
+        // 16-byte loads, same sequential fmaf order as the scalar loop (bit-identical result)
+        const float4* row = (const float4*)((const float*)a.x + (uint64_t)v * a.d);
+        for (uint32_t j4 = 0; j4 < (a.d >> 2); j4++) {
+            const float4 t = __ldg(row + j4);
+            const float* qq = qv + 4 * j4;
+            if (a.metric == SG_IP) {
+                s = __fmaf_rn(-t.x, qq[0], s); s = __fmaf_rn(-t.y, qq[1], s);
+                s = __fmaf_rn(-t.z, qq[2], s); s = __fmaf_rn(-t.w, qq[3], s);
+            } else {
+                s = __fmaf_rn(t.x - qq[0], t.x - qq[0], s); s = __fmaf_rn(t.y - qq[1], t.y - qq[1], s);
+                s = __fmaf_rn(t.z - qq[2], t.z - qq[2], s); s = __fmaf_rn(t.w - qq[3], t.w - qq[3], s);
+            }
+        }
     } else {
         const float* row = (const float*)a.x + (uint64_t)v * a.d;
         for (uint32_t j = 0; j < a.d; j++) {
