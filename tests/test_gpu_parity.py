@@ -270,6 +270,19 @@ def test_search_matches_oracle(api, oracle_mod):
     assert abs(rec - oracle_mod.recall(oo, ogt)) < 1e-12
 
 
+@pytest.mark.parametrize("d", [128, 40])
+def test_search_u8_matches_oracle(api, oracle_mod, d):
+    """u8 rows (BIGANN-shaped): the 16-byte load path (d = 128) and the scalar path (d = 40)
+    give the oracle's result lists."""
+    x = datagen.sift_like(3000, d, seed=45, as_u8=True)
+    ids, _ = oracle_mod.knn(x.numpy(), 16)
+    q = datagen.sift_like(100, d, seed=46, as_u8=True)
+    out, gt, rec = api.scalegann_search_eval(x.cuda(), torch.from_numpy(ids.view(np.int32)).cuda(), 0, q.cuda(),
+                                             topk=10, beam=32)
+    oo, _, _ = oracle_mod.search(x.numpy(), ids, 0, q.numpy(), topk=10, beam=32)
+    assert np.array_equal(u32(out), oo)
+
+
 def test_search_shards_split_only_matches_oracle(api, oracle_mod):
     """Split-only build (k = 3, omega = 1) searched per shard with result merge (P:432-470,
     reading R15): GPU == oracle list for list; per-shard search beats one global beam."""
