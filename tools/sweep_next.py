@@ -75,6 +75,20 @@ def main():
                                          "recall_at_10_beam64_per_shard_search": rec_sh})
         if omega == 2 and eps == 1.2:
             base = idx
+        if omega == 1:   # split-only: per-shard search throughput vs recall (QPS-matched comparison)
+            out["next2_split_only_search"] = []
+            for beam in (16, 32, 64):
+                api.scalegann_search_eval_shards(x, idx.merged, entries, q, topk=10, beam=beam, gt=gt)
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(3):
+                    _, _, r = api.scalegann_search_eval_shards(x, idx.merged, entries, q, topk=10, beam=beam, gt=gt)
+                e1.record()
+                torch.cuda.synchronize()
+                ms = e0.elapsed_time(e1) / 3
+                out["next2_split_only_search"].append({"beam_per_shard": beam, "recall_at_10": r,
+                                                       "ms_per_batch": ms, "qps": a.nq / (ms / 1000.0)})
         del idx
         torch.cuda.empty_cache()
 
