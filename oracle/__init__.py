@@ -52,6 +52,7 @@ def _load():
         _lib.oracle_knn.argtypes = [vp, vp, u64, vp, vp, u64, i32, u32, i32, u32, i32, vp, vp]
         _lib.oracle_prune.argtypes = [vp, vp, u64, u32, u32, i32, vp, vp]
         _lib.oracle_reverse.argtypes = [vp, vp, u64, u32, u32, vp, vp]
+        _lib.oracle_reverse_lists.argtypes = [vp, vp, u64, u32, vp, vp, vp]
         _lib.oracle_merge.argtypes = [vp, u64, u32, vp, vp, vp, vp, u32, vp, vp]
         _lib.oracle_entry_points.argtypes = [vp, vp, u64, u32, u32, vp, vp]
         _lib.oracle_entry_points.restype = u32
@@ -171,6 +172,19 @@ def reverse(pruned, pruned_d, protected=None):
     od = np.zeros((m, R), np.float32)
     _load().oracle_reverse(_p(pruned), _p(pruned_d), m, R, h, _p(out), _p(od))
     return out, od
+
+
+def reverse_lists(pruned, pruned_d):
+    """P6's rev[y] lists (reading R11): sources x in (k, x) order, capped at R.  Returns
+    (rev m x R SENT-padded, rev_d carried d(x -> y), counts)."""
+    pruned = np.ascontiguousarray(pruned, np.uint32)
+    pruned_d = np.ascontiguousarray(pruned_d, np.float32)
+    m, R = pruned.shape
+    rev = np.zeros((m, R), np.uint32)
+    rd = np.zeros((m, R), np.float32)
+    rc = np.zeros(m, np.uint32)
+    _load().oracle_reverse_lists(_p(pruned), _p(pruned_d), m, R, _p(rev), _p(rd), _p(rc))
+    return rev, rd, rc
 
 
 def merge(home, idmaps, graphs, graphs_d):

@@ -350,30 +350,43 @@ uint64_t oracle_idmap(const uint32_t* home, uint64_t n, uint32_t omega, uint32_t
 /* Exact kNN: for each row i of A, the L smallest (dist, j) over rows j of B,
  * j != i when self_exclude (A and B the same set).  ida/idb map local -> global
  * rows of the data arrays (NULL = identity).  Padded with (SENT, +inf). */
+/* (dist, id) order of cmp_pair as a predicate: a before b */
+static int pair_before(float da, uint32_t ia, float db, uint32_t ib) {
+    return da < db || (da == db && ia < ib);
+}
+
 void oracle_knn(const void* xa, const uint32_t* ida, uint64_t ma, const void* xb, const uint32_t* idb,
                 uint64_t mb, int dtype, uint32_t d, int self_exclude, uint32_t L, int metric,
                 uint32_t* out_ids, float* out_d) {
+    if (L == 0) return;
+    /* The L smallest (dist, j) are kept in a sorted list (insertion), which equals the
+     * first L entries of the fully sorted candidate list without sorting all mb of them. */
     #pragma omp parallel
     {
-        pair_t* buf = (pair_t*)malloc((mb + 1) * sizeof(pair_t));
+        pair_t* best = (pair_t*)malloc((L + 1) * sizeof(pair_t));
         #pragma omp for schedule(dynamic, 16)
         for (int64_t i = 0; i < (int64_t)ma; i++) {
             uint64_t ra = ida ? ida[i] : (uint64_t)i;
-            uint64_t cnt = 0;
+            uint32_t cnt = 0;
             for (uint64_t j = 0; j < mb; j++) {
                 if (self_exclude && j == (uint64_t)i) continue;
                 uint64_t rb = idb ? idb[j] : j;
-                buf[cnt].d = exact_dist(xa, ra, xb, rb, dtype, d, metric);
-                buf[cnt].id = (uint32_t)j;
-                cnt++;
+                float dj = exact_dist(xa, ra, xb, rb, dtype, d, metric);
+                if (cnt == L && !pair_before(dj, (uint32_t)j, best[L - 1].d, best[L - 1].id)) continue;
+                uint32_t p = cnt < L ? cnt++ : L - 1;      /* drop the current L-th when full */
+                while (p > 0 && pair_before(dj, (uint32_t)j, best[p - 1].d, best[p - 1].id)) {
+                    best[p] = best[p - 1];
+                    p--;
+                }
+                best[p].d = dj;
+                best[p].id = (uint32_t)j;
             }
-            qsort(buf, cnt, sizeof(pair_t), cmp_pair);
             for (uint32_t p = 0; p < L; p++) {
-                if (p < cnt) { out_ids[i * L + p] = buf[p].id; out_d[i * L + p] = buf[p].d; }
+                if (p < cnt) { out_ids[i * L + p] = best[p].id; out_d[i * L + p] = best[p].d; }
                 else { out_ids[i * L + p] = SENT; out_d[i * L + p] = INFINITY; }
             }
         }
-        free(buf);
+        free(best);
     }
 }
 
@@ -389,10 +402,16 @@ void oracle_prune(const uint32_t* knn, const float* knn_d, uint64_t m, uint32_t 
     {
         uint64_t* key = (uint64_t*)malloc(L * sizeof(uint64_t));
         uint32_t* cnt = (uint32_t*)malloc(L * sizeof(uint32_t));
+        /* rank_of[b] = r_ab for b in N[a] (first occurrence), SENT otherwise; set for the
+         * current a and cleared after it */
+        uint32_t* rank_of = (uint32_t*)malloc((m ? m : 1) * sizeof(uint32_t));
+        for (uint64_t b = 0; b < m; b++) rank_of[b] = SENT;
         #pragma omp for schedule(dynamic, 64)
         for (int64_t a = 0; a < (int64_t)m; a++) {
             const uint32_t* Na = knn + (uint64_t)a * L;
             memset(cnt, 0, L * sizeof(uint32_t));
+            for (uint32_t r = L; r-- > 0;)
+                if (Na[r] != SENT) rank_of[Na[r]] = r;
             for (uint32_t r_ad = 0; r_ad < L; r_ad++) {
                 uint32_t delta = Na[r_ad];
                 if (delta == SENT) continue;
@@ -400,14 +419,14 @@ void oracle_prune(const uint32_t* knn, const float* knn_d, uint64_t m, uint32_t 
                 for (uint32_t r_db = 0; r_db < L; r_db++) {
                     uint32_t b = Nd[r_db];
                     if (b == SENT || b == (uint32_t)a) continue;
-                    for (uint32_t r_ab = 0; r_ab < L; r_ab++) {
-                        if (Na[r_ab] != b) continue;
-                        uint32_t mx = rule == 0 ? (r_ad > r_db ? r_ad : r_db) : r_ad;
-                        if (mx < r_ab) cnt[r_ab]++;
-                        break;
-                    }
+                    uint32_t r_ab = rank_of[b];
+                    if (r_ab == SENT) continue;             /* b not in N[a] */
+                    uint32_t mx = rule == 0 ? (r_ad > r_db ? r_ad : r_db) : r_ad;
+                    if (mx < r_ab) cnt[r_ab]++;
                 }
             }
+            for (uint32_t r = 0; r < L; r++)
+                if (Na[r] != SENT) rank_of[Na[r]] = SENT;
             for (uint32_t r = 0; r < L; r++)
                 key[r] = Na[r] == SENT ? (0xFFFFFFFFull << 32) | r : ((uint64_t)cnt[r] << 32) | r;
             for (uint32_t i = 1; i < L; i++) {     /* stable insertion sort */
@@ -421,7 +440,7 @@ void oracle_prune(const uint32_t* knn, const float* knn_d, uint64_t m, uint32_t 
                 out_d[(uint64_t)a * R + i] = knn_d[(uint64_t)a * L + r];
             }
         }
-        free(key); free(cnt);
+        free(key); free(cnt); free(rank_of);
     }
 }
 
@@ -432,17 +451,26 @@ void oracle_prune(const uint32_t* knn, const float* knn_d, uint64_t m, uint32_t 
  * tail = rev_np ++ [f in pruned[y][h..R) : f not in rev_np],
  * out[y] = pruned[y][0..h) ++ tail[0..R-h).  A reverse edge y->x carries the
  * distance of x->y. */
-void oracle_reverse(const uint32_t* pruned, const float* pruned_d, uint64_t m, uint32_t R,
-                    uint32_t h, uint32_t* out, float* out_d) {
-    uint32_t* rev = (uint32_t*)malloc((size_t)m * R * sizeof(uint32_t));
-    float* rev_d = (float*)malloc((size_t)m * R * sizeof(float));
-    uint32_t* rc = (uint32_t*)calloc(m, sizeof(uint32_t));
+/* rev[y] (m x R, SENT padded) and |rev[y]| (rc) of reading R11: sources x in (k, x)
+ * order -- k outer, x inner -- appended while |rev[y]| < R; rev_d carries d(x -> y). */
+void oracle_reverse_lists(const uint32_t* pruned, const float* pruned_d, uint64_t m, uint32_t R,
+                          uint32_t* rev, float* rev_d, uint32_t* rc) {
+    for (uint64_t y = 0; y < m * R; y++) { rev[y] = SENT; rev_d[y] = INFINITY; }
+    memset(rc, 0, m * sizeof(uint32_t));
     for (uint32_t k = 0; k < R; k++)
         for (uint64_t x = 0; x < m; x++) {
             uint32_t y = pruned[x * R + k];
             if (y == SENT) continue;
             if (rc[y] < R) { rev[(uint64_t)y * R + rc[y]] = (uint32_t)x; rev_d[(uint64_t)y * R + rc[y]] = pruned_d[x * R + k]; rc[y]++; }
         }
+}
+
+void oracle_reverse(const uint32_t* pruned, const float* pruned_d, uint64_t m, uint32_t R,
+                    uint32_t h, uint32_t* out, float* out_d) {
+    uint32_t* rev = (uint32_t*)malloc((size_t)m * R * sizeof(uint32_t));
+    float* rev_d = (float*)malloc((size_t)m * R * sizeof(float));
+    uint32_t* rc = (uint32_t*)calloc(m, sizeof(uint32_t));
+    oracle_reverse_lists(pruned, pruned_d, m, R, rev, rev_d, rc);
     #pragma omp parallel
     {
         uint32_t* tail = (uint32_t*)malloc(2 * R * sizeof(uint32_t));
