@@ -30,7 +30,7 @@ constexpr uint32_t NTHREADS = 64 + NEPI * 32;
 constexpr uint32_t MAX_STAGES = 32;
 constexpr uint32_t NBUF_MAX = 4;         // TMEM buffers per accumulator: 4 (A in smem) or 2 (A in TMEM)
 constexpr uint32_t KSTRIDE = 36;         // floats per staged row (16B aligned, conflict-free)
-constexpr uint32_t SCRATCH = 32 * KSTRIDE * 4 + 64 * 4;   // per warp: staged keys | hist | sort buffer, + tile ids
+constexpr uint32_t SCRATCH = 32 * KSTRIDE * 4 + 64 * 4;   // per warp: staged keys | hist | sort buffer (+ spare)
 constexpr uint32_t SORT_MAX = 512;      // final sort buffer (u64 entries, aliases the staged keys)
 static_assert(SORT_MAX * 8 <= 32 * KSTRIDE * 4, "sort buffer exceeds the warp scratch");
 
@@ -116,15 +116,22 @@ __host__ __device__ constexpr uint32_t instr_desc() {
     return (1u << 4) | ((KIND ? 2u : 0u) << 7) | ((KIND ? 2u : 0u) << 10) | ((BN >> 3) << 17) | ((MSUB >> 4) << 24);
 }
 
-// (a - t, b - t) with one packed FADD2 (sm_100); results as raw bits
-__device__ __forceinline__ void sub2(uint32_t a, uint32_t b, float t, uint32_t& ra, uint32_t& rb) {
-    asm("{\n\t.reg .b64 x, y, z;\n\t"
-        "mov.b64 x, {%2, %3};\n\t"
-        "mov.b64 y, {%4, %4};\n\t"
-        "sub.rn.f32x2 z, x, y;\n\t"
-        "mov.b64 {%0, %1}, z;\n\t}"
-        : "=r"(ra), "=r"(rb)
-        : "r"(a), "r"(b), "r"(__float_as_uint(t)));
+__device__ __forceinline__ float min3f(float a, float b, float c) {   // one FMNMX3 (sm_100)
+    float r;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+// smallest of 32 keys (raw float bits): a depth-4 tree of 16 FMNMX3
+__device__ __forceinline__ float min32(const uint32_t (&v)[32]) {
+    float m[12];
+#pragma unroll
+    for (int i = 0; i < 10; i++)
+        m[i] = min3f(__uint_as_float(v[3 * i]), __uint_as_float(v[3 * i + 1]), __uint_as_float(v[3 * i + 2]));
+    m[10] = __uint_as_float(v[30]);
+    m[11] = __uint_as_float(v[31]);
+    const float a = min3f(m[0], m[1], m[2]), b = min3f(m[3], m[4], m[5]), c = min3f(m[6], m[7], m[8]),
+                d = min3f(m[9], m[10], m[11]);
+    return fminf(min3f(a, b, c), d);
 }
 
 __device__ __forceinline__ float next_up(float x) {   // smallest float > x (x < +inf)

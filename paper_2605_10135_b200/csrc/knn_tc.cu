@@ -34,6 +34,56 @@ namespace {
 // ----------------------------------------------------------------- the kernel
 constexpr uint32_t NEPI_R = 16;                         // epilogue warps (2 column streams x 8)
 constexpr uint32_t NTHREADS_R = 64 + NEPI_R * 32;
+static_assert(BN == 128, "the epilogue gives each column stream two 32-column passes per tile");
+
+constexpr uint32_t ROOM = 64;   // candidate-buffer slots a row may gain between compactions (one tile)
+
+// a row whose prefilter hit stages its 32 keys, its threshold and its next buffer slot
+__device__ __forceinline__ void stage_keys(float* skeys, uint32_t lane, const uint32_t (&v)[32], float te,
+                                           uint32_t slot) {
+    float4* st4 = (float4*)(skeys + lane * KSTRIDE);
+#pragma unroll
+    for (int j4 = 0; j4 < 8; j4++)
+        st4[j4] = make_float4(__uint_as_float(v[4 * j4]), __uint_as_float(v[4 * j4 + 1]), __uint_as_float(v[4 * j4 + 2]),
+                              __uint_as_float(v[4 * j4 + 3]));
+    *(float2*)(skeys + lane * KSTRIDE + 32) = make_float2(te, __uint_as_float(slot));
+}
+
+// The warp takes the staged rows of `hb` one at a time, lane j testing column col0 + j: one
+// ballot per row, the passing (key bits << 32 | id) words appended to consecutive slots of the
+// row's buffer.  Returns how many entries this lane's own row gained.
+__device__ __forceinline__ uint32_t insert_rows(const KnnParams& p, const float* skeys, uint32_t lane, uint32_t hb,
+                                                uint32_t col0, long long (&pw)[8]) {
+    const uint32_t myid = p.col_map ? __ldg(p.col_map + col0 + lane) : col0 + lane;
+    const uint32_t lt = (1u << lane) - 1u;
+    uint32_t add = 0;
+    if constexpr (SG_KNN_PROF != 0) pw[7] += __popc(hb);
+    do {
+        const int o = __ffs(hb) - 1;
+        hb &= hb - 1;
+        const float* ko = skeys + o * KSTRIDE;
+        const float kv = ko[lane];
+        const float2 tw = *(const float2*)(ko + 32);
+        const bool ps = kv < tw.x;   // key <= thr
+        const uint32_t b = __ballot_sync(0xffffffffu, ps);
+        if (ps) p.cand[__float_as_uint(tw.y) + __popc(b & lt)] = ((uint64_t)__float_as_uint(kv) << 32) | myid;
+        if (lane == (uint32_t)o) add = __popc(b);
+        if constexpr (SG_KNN_PROF != 0) pw[6] += __popc(b);
+    } while (hb);
+    return add;
+}
+
+// diagnostics instantiation: raw accumulator dump (probe) / keep the loads live (noepi)
+__device__ __forceinline__ void diag_pass(const KnnParams& p, const uint32_t (&v)[32], uint32_t col0, uint32_t row,
+                                          bool valid) {
+    if (p.noepi) {
+        if ((v[0] ^ v[31]) == 0x7fc00001u) p.out_ids[0] = v[1];
+    } else if (p.probe && valid) {
+#pragma unroll
+        for (int j = 0; j < 32; j++)
+            if (col0 + j < p.mb) p.probe[(uint64_t)row * p.mb + col0 + j] = __uint_as_float(v[j]);
+    }
+}
 
 // DIAG: the instantiation that honours the probe / diagnostics switches (raw accumulator dump,
 // stubbed epilogue, ablations); production launches use DIAG = false and skip those tests.
@@ -207,25 +257,30 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         const uint32_t e = warp - 2, s = e >> 3, q = warp & 3, a = (e & 7) >> 2;
         const uint32_t r = a * MSUB + q * 32 + lane;         // row within the block
         uint8_t* scratch = scratch_all + (s * 4 * NACC + (e & 7)) * SCRATCH;   // active warps only
-        float* skeys = (float*)scratch;                      // [32][KSTRIDE] staged keys
+        float* skeys = (float*)scratch;                      // [32][KSTRIDE] staged keys (+ te, slot)
         uint32_t* hist = (uint32_t*)scratch;                 // 256 (aliases skeys)
         uint64_t* sortbuf = (uint64_t*)scratch;              // 512 (aliases skeys)
-        uint32_t* sids = (uint32_t*)(scratch + 32 * KSTRIDE * 4);   // 64 reported ids of the tile
         const uint32_t C = p.C;
         const uint32_t keep_max = p.keep_max;                // in-loop compaction target (>= L)
         auto rowbuf = [&](uint32_t R, uint32_t st) -> uint64_t* {
             return p.cand + (((uint64_t)blockIdx.x * 2 + st) * BM + R) * C;
         };
-        uint64_t* myrow = rowbuf(r, s);
+        // word offset of this row's stream buffer from p.cand (the buffers span < 2^32 words)
+        const uint32_t mybase = (uint32_t)((((uint64_t)blockIdx.x * 2 + s) * BM + r) * C);
         uint64_t* warprows = rowbuf(a * MSUB + q * 32, s);
         const uint32_t tl = tmem + ((q * 32) << 16) + a * NBUF * BN;
         const uint64_t PINIT = pair_ord(3.40282347e38f, SG_SENT);   // every finite key passes, +inf not
         const uint32_t nbar = NACC * 8 * 32;                 // active epilogue threads
+        // extrapolated target rank per stream after tile ti: slope * (ti + 1) + beta
+        const float slope = p.alpha100 * 0.005f * (float)p.L * (float)BN / (float)p.mb;
+        // the self column is inserted like any other (its key is the row's smallest) and removed
+        // in the final phase; with plain rank-L thresholds it takes one of the kept ranks
+        const uint32_t want_full = p.L + (p.self_exclude ? 1u : 0u);
+        const uint32_t kmax_full = keep_max > want_full ? keep_max : want_full;
         uint32_t git = 0;
         for (uint32_t rb = blockIdx.x; rb < n_rb && a < NACC; rb += gridDim.x) {
             const uint32_t row = rb * RB + r;
             const bool valid = row < ma;
-            const uint32_t scol = p.self_exclude ? (p.self_col ? (valid ? p.self_col[row] : SG_SENT) : row) : SG_SENT;
             uint32_t cnt = 0;
             if (s == 0) s_pair[r] = valid ? PINIT : pair_ord(-__int_as_float(0x7f800000), 0);
             named_bar_sync(1, nbar);
@@ -237,124 +292,95 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 pw[0] += c1 - c0;
                 tc_fence_after();
                 const uint32_t tb = tl + buf * BN;
-                // the self column of some row of this block can only lie in a tile overlapping the
-                // block's own columns (or anywhere, for the fallback's explicit self columns)
-                const bool self_tile = p.self_exclude && (p.self_col || (t * BN < rb * RB + RB && rb * RB < t * BN + BN));
-                // the row threshold (possibly lowered by the other stream) for this tile
-                const float te = next_up(ord2f((uint32_t)(*(volatile unsigned long long*)&s_pair[r] >> 32)));
+                // the row threshold (possibly lowered by the other stream) for this tile:
+                // te = next_up(thr) is ord + 1 in the ordered key space, so key < te is key <= thr
+                float te = ord2f((uint32_t)(*(volatile unsigned long long*)&s_pair[r] >> 32) + 1u);
                 // compaction target rank per stream for this tile: L, or (extrapolated) the rank for
                 // the fraction of columns seen; trigger: buffer full, or `eager` above the target
-                uint32_t want = p.L, kmax = keep_max, trig = C - 32;
+                uint32_t want = want_full, kmax = kmax_full, trig = C - ROOM;
                 if (p.alpha100) {
-                    const float f = (float)((ti + 1) * BN) / (float)p.mb;
-                    const uint32_t rr = (uint32_t)(p.alpha100 * 0.005f * (float)p.L * f) + p.beta;
-                    if (rr < p.L) { want = rr; kmax = want + (C - 32 - want) / 8; }
+                    const uint32_t rr = (uint32_t)(slope * (float)(ti + 1)) + p.beta;
+                    if (rr < want) { want = rr; kmax = want + (C - ROOM - want) / 8; }
                     if (want + p.eager < trig) trig = want + p.eager;
                 }
-#pragma unroll 1
-                for (uint32_t hp = s * (BN / 64); hp < (s + 1) * (BN / 64); hp++) {   // this stream's passes
-                    uint32_t v[32];
-                    tmem_ld32_nowait(tb + hp * 32, v);
-                    tmem_wait_ld();
-                    if (hp == (s + 1) * (BN / 64) - 1) {
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(&bars->tm_empty[buf]);
-                    }
-                    c0 = clk();
-                    pw[1] += c0 - c1;
-                    const uint32_t col0 = t * BN + hp * 32;
-                    if (DIAG && p.noepi) {
-                        if ((v[0] ^ v[31]) == 0x7fc00001u) p.out_ids[0] = v[1];   // keep the loads live
-                        continue;
-                    }
-                    if (DIAG && p.probe) {
-                        if (valid) {
-#pragma unroll
-                            for (int j = 0; j < 32; j++)
-                                if (col0 + j < p.mb) p.probe[(uint64_t)row * p.mb + col0 + j] = __uint_as_float(v[j]);
-                        }
-                        continue;
-                    }
-                    // pass mask: bit j set iff key(j) < te, i.e. key(j) <= thr
-                    uint32_t mq[4] = {0, 0, 0, 0};
-#pragma unroll
-                    for (int s2 = 7; s2 >= 1; s2 -= 2) {
-#pragma unroll
-                        for (int g = 0; g < 4; g++) {
-                            const int j = g * 8 + s2;
-                            uint32_t lo, hi;
-                            sub2(v[j - 1], v[j], te, lo, hi);
-                            mq[g] = __funnelshift_l(hi, mq[g], 1);
-                            mq[g] = __funnelshift_l(lo, mq[g], 1);
-                        }
-                    }
-                    uint32_t m = mq[0] | (mq[1] << 8) | (mq[2] << 16) | (mq[3] << 24);
-                    if (self_tile && scol - col0 < 32u) m &= ~(1u << (scol - col0));   // self column
-                    c1 = clk();
-                    pw[3] += c1 - c0;
-                    if (DIAG && (p.abl & 1)) m = 0;
-                    if (__any_sync(0xffffffffu, m != 0)) {
-                        sids[lane] = p.col_map ? __ldg(p.col_map + col0 + lane) : col0 + lane;
-                        float4* st4 = (float4*)(skeys + lane * KSTRIDE);
-#pragma unroll
-                        for (int j4 = 0; j4 < 8; j4++)
-                            st4[j4] = make_float4(__uint_as_float(v[4 * j4]), __uint_as_float(v[4 * j4 + 1]),
-                                                  __uint_as_float(v[4 * j4 + 2]), __uint_as_float(v[4 * j4 + 3]));
-                        __syncwarp();
-                        if constexpr (PROF) pw[6] += __popc(m);
-                        const float* mykeys = skeys + lane * KSTRIDE;
-                        while (m) {   // two candidates per iteration
-                            if constexpr (PROF) pw[7]++;
-                            const uint32_t b0 = 31 - __clz(m);
-                            m ^= 1u << b0;
-                            const bool two = m != 0;
-                            const uint32_t b1 = two ? 31 - __clz(m) : b0;
-                            m &= ~(1u << b1);
-                            const uint32_t k0 = __float_as_uint(mykeys[b0]), i0 = sids[b0];
-                            const uint32_t k1 = __float_as_uint(mykeys[b1]), i1 = sids[b1];
-                            myrow[cnt] = ((uint64_t)k0 << 32) | i0;
-                            if (two) myrow[cnt + 1] = ((uint64_t)k1 << 32) | i1;
-                            cnt += two ? 2 : 1;
-                        }
-                        __syncwarp();
-                    }
-                    c0 = clk();
-                    pw[4] += c0 - c1;
-                    // make room: compact rows whose buffer cannot take another pass to the target
-                    // rank per stream (L, or the extrapolated rank for the fraction seen) under the
-                    // row threshold, and lower the shared pair
-                    // (extrapolated mode: also eagerly, once a stream holds `eager` entries above its
-                    // target rank, so the shared threshold follows the fraction of columns seen)
-                    uint32_t need = __ballot_sync(0xffffffffu, cnt > trig);
-                    if (need) {
-                        do {
-                            const int o = __ffs(need) - 1;
-                            need &= need - 1;
-                            const uint32_t c_o = __shfl_sync(0xffffffffu, cnt, o);
-                            const uint32_t R = a * MSUB + q * 32 + o;
-                            uint64_t* ob = warprows + (uint64_t)o * C;
-                            const uint64_t cap = *(volatile unsigned long long*)&s_pair[R];
-                            uint32_t kept;
-                            uint64_t P = select_pairs<EPL>(ob, c_o, cap, want, kmax, lane, &kept);
-                            if (kept > C - 32)   // massive ties on the threshold key: split them by id
-                                P = select_L<EPL>(ob, kept, want, kmax, hist, lane, &kept);
-                            if (lane == (uint32_t)o) {
-                                cnt = kept;
-                                atomicMin(&s_pair[R], (unsigned long long)P);
-                            }
-                        } while (need);
-                    }
-                    c1 = clk();
-                    pw[2] += c1 - c0;
+                // this stream's two 32-column passes.  One TMEM load each (18 warps leave 96
+                // registers per thread, too few to hold both); the rows whose prefilter hits stage
+                // pass 0's keys in shared memory so that pass 1 is loaded and the buffer handed
+                // back to the MMA before any insertion or compaction work
+                const uint32_t cb = t * BN + s * 64;   // first column of pass 0
+                uint32_t vv[32];
+                tmem_ld32_nowait(tb + s * 64, vv);
+                tmem_wait_ld();
+                c0 = clk();
+                pw[1] += c0 - c1;
+                bool hit = min32(vv) < te;   // prefilter: smallest key of the pass vs the threshold
+                uint32_t hb0 = __ballot_sync(0xffffffffu, hit);
+                if (hit) stage_keys(skeys, lane, vv, te, mybase + cnt);
+                if (DIAG) diag_pass(p, vv, cb, row, valid);
+                c1 = clk();
+                pw[3] += c1 - c0;
+                tmem_ld32_nowait(tb + s * 64 + 32, vv);
+                tmem_wait_ld();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->tm_empty[buf]);
+                c0 = clk();
+                pw[1] += c0 - c1;
+                hit = min32(vv) < te;
+                uint32_t hb1 = __ballot_sync(0xffffffffu, hit);
+                if (DIAG) {
+                    diag_pass(p, vv, cb + 32, row, valid);
+                    if (p.noepi || p.probe || (p.abl & 1)) hb0 = hb1 = 0;
                 }
+                c1 = clk();
+                pw[3] += c1 - c0;
+                if (hb0) {
+                    __syncwarp();
+                    cnt += insert_rows(p, skeys, lane, hb0, cb, pw);
+                }
+                if (hb1) {
+                    __syncwarp();   // pass 0's staged keys are consumed
+                    if (hit) stage_keys(skeys, lane, vv, te, mybase + cnt);
+                    __syncwarp();
+                    cnt += insert_rows(p, skeys, lane, hb1, cb + 32, pw);
+                }
+                c0 = clk();
+                pw[4] += c0 - c1;
+                // make room for the next tile (<= ROOM more entries): compact rows whose buffer
+                // passed the trigger to the target rank per stream (L, or the extrapolated rank
+                // for the fraction seen) under the row threshold, and lower the shared pair
+                // (extrapolated mode: also eagerly, once a stream holds `eager` entries above its
+                // target rank, so the shared threshold follows the fraction of columns seen)
+                uint32_t need = __ballot_sync(0xffffffffu, cnt > trig);
+                if (need) {
+                    do {
+                        const int o = __ffs(need) - 1;
+                        need &= need - 1;
+                        const uint32_t c_o = __shfl_sync(0xffffffffu, cnt, o);
+                        const uint32_t R = a * MSUB + q * 32 + o;
+                        uint64_t* ob = warprows + (uint64_t)o * C;
+                        const uint64_t cap = *(volatile unsigned long long*)&s_pair[R];
+                        uint32_t kept;
+                        uint64_t P = select_pairs<EPL>(ob, c_o, cap, want, kmax, lane, &kept);
+                        if (kept > C - ROOM)   // massive ties on the threshold key: split them by id
+                            P = select_L<EPL>(ob, kept, want, kmax, hist, lane, &kept);
+                        if (lane == (uint32_t)o) {
+                            cnt = kept;
+                            atomicMin(&s_pair[R], (unsigned long long)P);
+                            te = ord2f((uint32_t)(P >> 32) + 1u);
+                        }
+                    } while (need);
+                }
+                c1 = clk();
+                pw[2] += c1 - c0;
             }
             if (DIAG && (p.probe || p.noepi)) continue;
             const long long f0 = clk();
             s_cnt[s][r] = cnt;
             named_bar_sync(1, nbar);
-            // ---- final: union of the row's two stream buffers, exactness check, sorted top-L;
-            //      the 32 rows of this (q, a) group are split between its two stream warps
+            // ---- final: union of the row's two stream buffers without the self column, exactness
+            //      check, sorted top-L; the 32 rows of this (q, a) group are split between its two
+            //      stream warps
             for (uint32_t o = 16 * s; o < 16 * s + 16; o++) {
                 const uint32_t R = a * MSUB + q * 32 + o;
                 const uint32_t row_o = rb * RB + R;
@@ -362,6 +388,27 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 const uint64_t P = s_pair[R];
                 uint64_t* bb[2] = {rowbuf(R, 0), rowbuf(R, 1)};
                 uint32_t cc[2] = {s_cnt[0][R], s_cnt[1][R]};
+                if (p.self_exclude) {
+                    // reported id of the self column; at most one entry carries it
+                    const uint32_t sc = p.self_col ? p.self_col[row_o] : row_o;
+                    const uint32_t sid = p.col_map ? p.col_map[sc] : sc;
+#pragma unroll
+                    for (int st = 0; st < 2; st++) {
+                        for (uint32_t i0 = 0; i0 < cc[st]; i0 += 32) {
+                            const uint32_t i = i0 + lane;
+                            const uint32_t f = __ballot_sync(0xffffffffu, i < cc[st] && (uint32_t)bb[st][i] == sid);
+                            if (f) {
+                                const uint32_t at = i0 + __ffs(f) - 1;
+                                const uint64_t last = bb[st][cc[st] - 1];
+                                __syncwarp();
+                                if (lane == 0) bb[st][at] = last;
+                                __syncwarp();
+                                cc[st]--;
+                                break;
+                            }
+                        }
+                    }
+                }
                 uint32_t n_le = 0;
 #pragma unroll
                 for (int st = 0; st < 2; st++) {
@@ -410,13 +457,13 @@ uint32_t cand_cap(uint32_t L) {
     uint32_t c = 256;
     while (c < 2 * L && c < 1024) c <<= 1;
     if (env > 0) c = (uint32_t)env < 1024u ? (uint32_t)env : 1024u;
-    while (c < L + 64) c <<= 1;
+    while (c < L + 2 * ROOM) c <<= 1;   // the trigger C - ROOM stays above the kept set (>= L + 1)
     return c;
 }
 uint32_t keep_target(uint32_t L, uint32_t C) {
     static int env = -1;
     if (env < 0) { const char* e = getenv("SG_KNN_KEEP"); env = e ? atoi(e) : 0; }
-    return env == 1 ? L : L + (C - 32 - L) / 8;
+    return env == 1 ? L : L + (C - ROOM - L) / 8;
 }
 
 template <int KIND, int NKA, int MINI, int EPL>
