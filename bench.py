@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-recall", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the oracle parity check at bench size")
     ap.add_argument("--profile-steps", action="store_true", help="minimal run for ncu (no e2e/cpu/recall)")
     return ap.parse_args()
 
@@ -142,6 +143,80 @@ def oracle_sample_run(x_np, C_np, k, omega, L, sample_rows, home_np=None):
             f"against the whole shard ({k} shards), extrapolated x m/{sample_rows}; prune/reverse/merge "
             f"(O(m L^2), <2% of the oracle's kNN work) not timed")
     return t_part + t_knn_ex, t_part + t_knn, desc
+
+
+def oracle_rows_exact(oracle, x_np, rows, idb, L):
+    """P4 top-L of shard rows `rows` (local ids into idb) against the whole shard, self excluded:
+    the oracle's top L+1 with the self column included, minus self (if self is not among them,
+    >= L+1 exact duplicates with lower ids precede it and the first L are the answer)."""
+    import numpy as np
+    ids, dd = oracle.knn(x_np, L + 1, ida=idb[rows].astype(np.uint32), xb=x_np, idb=idb, self_exclude=False)
+    out_i = np.zeros((len(rows), L), np.uint32)
+    out_d = np.zeros((len(rows), L), np.float32)
+    for t, r in enumerate(rows):
+        keep = ids[t] != r
+        if keep.all():
+            keep[-1] = False
+        out_i[t], out_d[t] = ids[t][keep], dd[t][keep]
+    return out_i, out_d
+
+
+def scale_parity(x, idx, cfg, sample_rows=2000, seed=5):
+    """Parity at the bench's own size (after the timed region, in the oracle leg):
+      * partition: the oracle's home[] from the library's centroids equals the GPU's, bit for bit;
+      * kNN: `sample_rows` rows of the largest shard (first rows, last rows = ragged tail, random)
+        have exactly the oracle's P4 top-L (ids and dists);
+      * prune + reverse + merge: the oracle fed the GPU's kNN lists of every shard rebuilds the
+        merged graph, which must equal the GPU's merged graph byte for byte.
+    Returns a dict for the bench line."""
+    import numpy as np
+    import oracle
+    from paper_2605_10135_b200 import api
+    oracle.build()
+    t0 = time.perf_counter()
+    x_np = x.cpu().numpy()
+    r = oracle.partition(x_np, idx.centroids.cpu().numpy(), omega=cfg.omega, eps=cfg.epsilon,
+                         theta0_ppm=cfg.theta0_ppm, alpha=cfg.alpha, block_size=cfg.block_size)
+    home_gpu = idx.home.cpu().numpy().view(np.uint32)
+    home_ok = bool(np.array_equal(home_gpu, r["home"]))
+    big = max(range(cfg.k), key=lambda s: (idx.sizes[s], -s))
+    idm, gs, gds = [], [], []
+    knn_rows_ok = knn_rows = 0
+    for s in range(cfg.k):
+        im = oracle.idmap(r["home"], s)
+        im_d = torch_from(im, x.device)
+        g, gd, kid, kd = api.scalegann_build_shard(x, im_d, cfg.L, cfg.R, keep_knn=True)
+        kid_h = kid.cpu().numpy().view(np.uint32)
+        kd_h = kd.cpu().numpy()
+        del g, gd, kid, kd
+        if s == big:
+            m = len(im)
+            rng = np.random.default_rng(seed)
+            rows = sorted(set(range(min(m, 200))) | set(range(max(0, m - 300), m)) |
+                          set(rng.choice(m, size=min(m, max(0, sample_rows - 500)), replace=False).tolist()))
+            rows = np.array(rows, np.int64)
+            oi, od = oracle_rows_exact(oracle, x_np, rows, im, cfg.L)
+            same = (kid_h[rows] == oi).all(1) & (kd_h[rows] == od).all(1)
+            knn_rows, knn_rows_ok = len(rows), int(same.sum())
+        p, pd = oracle.prune(kid_h, kd_h, cfg.R, rule=cfg.prune_rule)
+        f, fd = oracle.reverse(p, pd, protected=cfg.protected_edges or None)
+        idm.append(im), gs.append(f), gds.append(fd)
+    om, omd = oracle.merge(r["home"], idm, gs, gds)
+    merged = idx.merged.cpu().numpy().view(np.uint32)
+    merged_ok = bool(np.array_equal(merged, om) and np.array_equal(idx.merged_d.cpu().numpy(), omd))
+    return {"home_identical": home_ok,
+            "knn_sampled_rows": knn_rows, "knn_rows_identical": knn_rows_ok,
+            "knn_sample": f"largest shard ({idx.sizes[big]} rows): first 200, last 300, "
+                          f"{max(0, sample_rows - 500)} random rows vs the oracle's exact P4 top-{cfg.L}",
+            "replay_merged_identical": merged_ok,
+            "replay": "oracle prune + reverse + merge fed the GPU kNN lists of every shard vs the GPU merged graph",
+            "seconds": time.perf_counter() - t0}
+
+
+def torch_from(a, device):
+    import numpy as np
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int32)).to(device)
 
 
 def run_reference(args):
@@ -332,6 +407,7 @@ def main():
 
     # ---------------- CPU oracle baseline (rank 0, N=1 only, bounded sample)
     cpu = None
+    parity = None
     if not args.no_cpu_baseline and world == 1 and rank == 0:
         import oracle
         oracle.build()
@@ -339,6 +415,8 @@ def main():
         ext, meas, desc = oracle_sample_run(x.cpu().numpy(), idx.centroids.cpu().numpy(), k, 2, 128, sample)
         cpu = {"value": n / ext, "unit": UNIT, "cores": cores(), "kind": "oracle", "sample": desc,
                "measured_s": meas, "extrapolated_s": ext}
+        if not args.no_parity:
+            parity = scale_parity(x, idx, cfg)
 
     if rank == 0:
         line = {
@@ -353,9 +431,7 @@ def main():
                        "parallelism": f"shard-parallel x{world} (LPT on m^2), NCCL bcast + all-to-all"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks, "recall_at_10": recall,
-            "recall_vs_oracle": "identical graph: on this integer data every stage is bit-exact with the "
-                                "oracle (tests/test_gpu_parity.py::test_end_to_end_integer_bit_exact, "
-                                "__graft_entry__.smoke), so the oracle-built graph has the same recall",
+            "parity_at_scale": parity,
             "stage_ms_untimed_step": stage_ms,
         }
         emit(line)

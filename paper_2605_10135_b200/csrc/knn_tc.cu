@@ -58,17 +58,25 @@ __device__ __forceinline__ uint32_t insert_rows(const KnnParams& p, const float*
     const uint32_t lt = (1u << lane) - 1u;
     uint32_t add = 0;
     if constexpr (SG_KNN_PROF != 0) pw[7] += __popc(hb);
-    do {
-        const int o = __ffs(hb) - 1;
+    do {   // two rows per iteration: independent load -> compare -> ballot -> store chains
+        const int o1 = __ffs(hb) - 1;
         hb &= hb - 1;
-        const float* ko = skeys + o * KSTRIDE;
-        const float kv = ko[lane];
-        const float2 tw = *(const float2*)(ko + 32);
-        const bool ps = kv < tw.x;   // key <= thr
-        const uint32_t b = __ballot_sync(0xffffffffu, ps);
-        if (ps) p.cand[__float_as_uint(tw.y) + __popc(b & lt)] = ((uint64_t)__float_as_uint(kv) << 32) | myid;
-        if (lane == (uint32_t)o) add = __popc(b);
-        if constexpr (SG_KNN_PROF != 0) pw[6] += __popc(b);
+        const bool two = hb != 0;
+        const int o2 = two ? __ffs(hb) - 1 : o1;
+        hb &= hb - 1;
+        const float* k1 = skeys + o1 * KSTRIDE;
+        const float* k2 = skeys + o2 * KSTRIDE;
+        const float kv1 = k1[lane], kv2 = k2[lane];
+        const float2 tw1 = *(const float2*)(k1 + 32), tw2 = *(const float2*)(k2 + 32);
+        const bool ps1 = kv1 < tw1.x;           // key <= thr
+        const bool ps2 = two && kv2 < tw2.x;
+        const uint32_t b1 = __ballot_sync(0xffffffffu, ps1);
+        const uint32_t b2 = __ballot_sync(0xffffffffu, ps2);
+        if (ps1) p.cand[__float_as_uint(tw1.y) + __popc(b1 & lt)] = ((uint64_t)__float_as_uint(kv1) << 32) | myid;
+        if (ps2) p.cand[__float_as_uint(tw2.y) + __popc(b2 & lt)] = ((uint64_t)__float_as_uint(kv2) << 32) | myid;
+        add = lane == (uint32_t)o1 ? __popc(b1) : add;
+        add = lane == (uint32_t)o2 && two ? __popc(b2) : add;
+        if constexpr (SG_KNN_PROF != 0) pw[6] += __popc(b1) + __popc(b2);
     } while (hb);
     return add;
 }
