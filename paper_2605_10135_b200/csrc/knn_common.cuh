@@ -152,7 +152,8 @@ struct KnnParams {
     const uint32_t* col_map;   // B row (operand order) -> reported id (nullptr = identity)
     uint32_t ma, mb, L, C, n_rb, n_ct, stages;
     uint32_t keep_max;         // in-loop compaction keeps between L and keep_max candidates
-    uint32_t nka;              // streamed-A kernel: full 128-byte K atoms per row (run time)
+    uint32_t nka;              // streamed-A / pair kernels: full 128-byte K atoms per row (run time)
+    uint32_t mini;             // pair kernel: 1 if a 32-byte K-tail atom follows
     // Extrapolated thresholds (columns in id order, no rotation): after `seen` of mb columns the
     // in-loop compaction keeps rank r = min(L, alpha100 * L * seen / (100 mb) + beta) instead of L.
     // The buffer always holds every seen column with (key, id) <= the threshold entry, so a row
@@ -427,14 +428,61 @@ __device__ __forceinline__ uint64_t select_pairs(uint64_t* rb, uint32_t cnt, uin
     return P;
 }
 
-// Union of two candidate lists: selected down to the keys <= the L-th smallest key in shared
+// a row whose prefilter hit stages its 32 keys, its threshold and its next buffer slot
+__device__ __forceinline__ void stage_keys(float* skeys, uint32_t lane, const uint32_t (&v)[32], float te,
+                                           uint32_t slot) {
+    float4* st4 = (float4*)(skeys + lane * KSTRIDE);
+#pragma unroll
+    for (int j4 = 0; j4 < 8; j4++)
+        st4[j4] = make_float4(__uint_as_float(v[4 * j4]), __uint_as_float(v[4 * j4 + 1]), __uint_as_float(v[4 * j4 + 2]),
+                              __uint_as_float(v[4 * j4 + 3]));
+    *(float2*)(skeys + lane * KSTRIDE + 32) = make_float2(te, __uint_as_float(slot));
+}
+
+// The warp takes the staged rows of `hb` one at a time, lane j testing column col0 + j: one
+// ballot per row, the passing (key bits << 32 | id) words appended to consecutive slots of the
+// row's buffer.  Returns how many entries this lane's own row gained.
+__device__ __forceinline__ uint32_t insert_rows(const KnnParams& p, const float* skeys, uint32_t lane, uint32_t hb,
+                                                uint32_t col0, long long (&pw)[8]) {
+    const uint32_t myid = p.col_map ? __ldg(p.col_map + col0 + lane) : col0 + lane;
+    const uint32_t lt = (1u << lane) - 1u;
+    uint32_t add = 0;
+    if constexpr (SG_KNN_PROF != 0) pw[7] += __popc(hb);
+    do {   // two rows per iteration: independent load -> compare -> ballot -> store chains
+        const int o1 = __ffs(hb) - 1;
+        hb &= hb - 1;
+        const bool two = hb != 0;
+        const int o2 = two ? __ffs(hb) - 1 : o1;
+        hb &= hb - 1;
+        const float* k1 = skeys + o1 * KSTRIDE;
+        const float* k2 = skeys + o2 * KSTRIDE;
+        const float kv1 = k1[lane], kv2 = k2[lane];
+        const float2 tw1 = *(const float2*)(k1 + 32), tw2 = *(const float2*)(k2 + 32);
+        const bool ps1 = kv1 < tw1.x;           // key <= thr
+        const bool ps2 = two && kv2 < tw2.x;
+        const uint32_t b1 = __ballot_sync(0xffffffffu, ps1);
+        const uint32_t b2 = __ballot_sync(0xffffffffu, ps2);
+        if (ps1) p.cand[__float_as_uint(tw1.y) + __popc(b1 & lt)] = ((uint64_t)__float_as_uint(kv1) << 32) | myid;
+        if (ps2) p.cand[__float_as_uint(tw2.y) + __popc(b2 & lt)] = ((uint64_t)__float_as_uint(kv2) << 32) | myid;
+        add = lane == (uint32_t)o1 ? __popc(b1) : add;
+        add = lane == (uint32_t)o2 && two ? __popc(b2) : add;
+        if constexpr (SG_KNN_PROF != 0) pw[6] += __popc(b1) + __popc(b2);
+    } while (hb);
+    return add;
+}
+
+// Union of NL candidate lists: selected down to the keys <= the L-th smallest key in shared
 // memory first (ties kept), then sorted by (dist, id) with dist = |a_i|^2 + key; first L written
-// (sentinel / +inf padding).  sortbuf holds SORT_MAX words; c0 + c1 <= SORT_MAX.
-template <int EPL_S>
-__device__ void finish_union(const uint64_t* b0, uint32_t c0, const uint64_t* b1, uint32_t c1, uint32_t L,
-                             uint64_t* sortbuf, float na, uint32_t* out_ids, float* out_d, uint32_t lane) {
-    uint32_t cnt = c0 + c1;
-    for (uint32_t p = lane; p < cnt; p += 32) sortbuf[p] = p < c0 ? b0[p] : b1[p - c0];
+// (sentinel / +inf padding).  sortbuf holds SORT_MAX words; the counts sum to <= SORT_MAX.
+template <int EPL_S, int NL>
+__device__ void finish_union_n(const uint64_t* const (&b)[NL], const uint32_t (&c)[NL], uint32_t L, uint64_t* sortbuf,
+                               float na, uint32_t* out_ids, float* out_d, uint32_t lane) {
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int k = 0; k < NL; k++) {
+        for (uint32_t p = lane; p < c[k]; p += 32) sortbuf[cnt + p] = b[k][p];
+        cnt += c[k];
+    }
     __syncwarp();
     if (cnt > L) select_keys<EPL_S>(sortbuf, cnt, L, L, lane, &cnt);
     uint32_t np = 32;
@@ -456,6 +504,13 @@ __device__ void finish_union(const uint64_t* b0, uint32_t c0, const uint64_t* b1
         out_d[p] = p < cnt ? ord2f((uint32_t)(w >> 32)) : __int_as_float(0x7f800000);
     }
     __syncwarp();
+}
+template <int EPL_S>
+__device__ void finish_union(const uint64_t* b0, uint32_t c0, const uint64_t* b1, uint32_t c1, uint32_t L,
+                             uint64_t* sortbuf, float na, uint32_t* out_ids, float* out_d, uint32_t lane) {
+    const uint64_t* const b[2] = {b0, b1};
+    const uint32_t c[2] = {c0, c1};
+    finish_union_n<EPL_S, 2>(b, c, L, sortbuf, na, out_ids, out_d, lane);
 }
 
 // Merge the two column halves' survivors of one row (each <= L), sort by (dist, id) with

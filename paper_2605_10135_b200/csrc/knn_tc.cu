@@ -38,49 +38,6 @@ static_assert(BN == 128, "the epilogue gives each column stream two 32-column pa
 
 constexpr uint32_t ROOM = 64;   // candidate-buffer slots a row may gain between compactions (one tile)
 
-// a row whose prefilter hit stages its 32 keys, its threshold and its next buffer slot
-__device__ __forceinline__ void stage_keys(float* skeys, uint32_t lane, const uint32_t (&v)[32], float te,
-                                           uint32_t slot) {
-    float4* st4 = (float4*)(skeys + lane * KSTRIDE);
-#pragma unroll
-    for (int j4 = 0; j4 < 8; j4++)
-        st4[j4] = make_float4(__uint_as_float(v[4 * j4]), __uint_as_float(v[4 * j4 + 1]), __uint_as_float(v[4 * j4 + 2]),
-                              __uint_as_float(v[4 * j4 + 3]));
-    *(float2*)(skeys + lane * KSTRIDE + 32) = make_float2(te, __uint_as_float(slot));
-}
-
-// The warp takes the staged rows of `hb` one at a time, lane j testing column col0 + j: one
-// ballot per row, the passing (key bits << 32 | id) words appended to consecutive slots of the
-// row's buffer.  Returns how many entries this lane's own row gained.
-__device__ __forceinline__ uint32_t insert_rows(const KnnParams& p, const float* skeys, uint32_t lane, uint32_t hb,
-                                                uint32_t col0, long long (&pw)[8]) {
-    const uint32_t myid = p.col_map ? __ldg(p.col_map + col0 + lane) : col0 + lane;
-    const uint32_t lt = (1u << lane) - 1u;
-    uint32_t add = 0;
-    if constexpr (SG_KNN_PROF != 0) pw[7] += __popc(hb);
-    do {   // two rows per iteration: independent load -> compare -> ballot -> store chains
-        const int o1 = __ffs(hb) - 1;
-        hb &= hb - 1;
-        const bool two = hb != 0;
-        const int o2 = two ? __ffs(hb) - 1 : o1;
-        hb &= hb - 1;
-        const float* k1 = skeys + o1 * KSTRIDE;
-        const float* k2 = skeys + o2 * KSTRIDE;
-        const float kv1 = k1[lane], kv2 = k2[lane];
-        const float2 tw1 = *(const float2*)(k1 + 32), tw2 = *(const float2*)(k2 + 32);
-        const bool ps1 = kv1 < tw1.x;           // key <= thr
-        const bool ps2 = two && kv2 < tw2.x;
-        const uint32_t b1 = __ballot_sync(0xffffffffu, ps1);
-        const uint32_t b2 = __ballot_sync(0xffffffffu, ps2);
-        if (ps1) p.cand[__float_as_uint(tw1.y) + __popc(b1 & lt)] = ((uint64_t)__float_as_uint(kv1) << 32) | myid;
-        if (ps2) p.cand[__float_as_uint(tw2.y) + __popc(b2 & lt)] = ((uint64_t)__float_as_uint(kv2) << 32) | myid;
-        add = lane == (uint32_t)o1 ? __popc(b1) : add;
-        add = lane == (uint32_t)o2 && two ? __popc(b2) : add;
-        if constexpr (SG_KNN_PROF != 0) pw[6] += __popc(b1) + __popc(b2);
-    } while (hb);
-    return add;
-}
-
 // diagnostics instantiation: raw accumulator dump (probe) / keep the loads live (noepi)
 __device__ __forceinline__ void diag_pass(const KnnParams& p, const uint32_t (&v)[32], uint32_t col0, uint32_t row,
                                           bool valid) {
@@ -457,7 +414,9 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     }
 }
 
-// Candidate buffer words per row: room for one 32-column pass above the kept set (>= L + 32).
+}  // namespace
+
+// Candidate buffer words per row: room for one tile above the kept set (>= L + 2 ROOM).
 // SG_KNN_C overrides (tuning); SG_KNN_KEEP=1 makes in-loop compaction exact (keep L).
 uint32_t cand_cap(uint32_t L) {
     static int env = -1;
@@ -468,6 +427,8 @@ uint32_t cand_cap(uint32_t L) {
     while (c < L + 2 * ROOM) c <<= 1;   // the trigger C - ROOM stays above the kept set (>= L + 1)
     return c;
 }
+
+namespace {
 uint32_t keep_target(uint32_t L, uint32_t C) {
     static int env = -1;
     if (env < 0) { const char* e = getenv("SG_KNN_KEEP"); env = e ? atoi(e) : 0; }
@@ -536,6 +497,8 @@ uint32_t knn_row_align() { return BM; }
 // transposed kernel (knn_tct.cu): L <= 128, selected unless SG_KNN_T=0
 uint32_t knn_t_cap(uint32_t L, bool extrap);
 sg_status launch_knn_t(const CUtensorMap* maps, KnnParams& p, int esize, int nka, int mini, cudaStream_t st);
+bool knn2_supported(uint32_t nka, uint32_t L, bool probe);
+sg_status launch_knn2(const CUtensorMap* maps, KnnParams& p, int esize, int nka, int mini, cudaStream_t st);
 static bool use_transposed(uint32_t L) {
     static int on = -1;
     if (on < 0) { const char* e = getenv("SG_KNN_T"); on = e ? atoi(e) : 0; }
@@ -576,6 +539,19 @@ int env_int(const char* name, int dflt) {
 
 sg_status launch_knn(const Operand& A, const Operand& B, KnnParams& p, cudaStream_t st) {
     CUtensorMap maps[4];
+    if (!use_transposed(p.L) && knn2_supported(A.nfull, p.L, p.probe != nullptr)) {
+        // CTA-pair kernel (knn_tc2.cu): each CTA loads 64 of every 128 B-tile rows
+        SG_TRY(make_map(&maps[0], A.a, A.rows_pad, A.kdim, A.esize, 128, MSUB));
+        SG_TRY(make_map(&maps[1], B.b, B.rows_pad, B.kdim, B.esize, 128, BN / 2));
+        if (A.mini) {
+            SG_TRY(make_map(&maps[2], A.a, A.rows_pad, A.kdim, A.esize, 32, MSUB));
+            SG_TRY(make_map(&maps[3], B.b, B.rows_pad, B.kdim, B.esize, 32, BN / 2));
+        } else {
+            maps[2] = maps[0];
+            maps[3] = maps[1];
+        }
+        return launch_knn2(maps, p, (int)A.esize, (int)A.nfull, (int)A.mini, st);
+    }
     SG_TRY(make_map(&maps[0], A.a, A.rows_pad, A.kdim, A.esize, 128, MSUB));
     SG_TRY(make_map(&maps[1], B.b, B.rows_pad, B.kdim, B.esize, 128, BN));
     if (A.mini) {
@@ -651,7 +627,7 @@ sg_status knn_core(const Operand& A, const Operand& B, int /*metric*/, bool self
     if (!cv.ok()) { set_error("kNN: workspace too small (fallback)"); return SG_ERR_WORKSPACE; }
     SG_CUDA(cudaMemsetAsync(fail_count, 0, sizeof(uint32_t), st));
     p.alpha100 = (uint32_t)alpha;
-    p.beta = (uint32_t)(beta >= 0 ? beta : tr ? 6 : 12);   // per column stream
+    p.beta = (uint32_t)(beta >= 0 ? beta : tr ? 6 : knn2_supported(A.nfull, L, false) ? 8 : 12);   // per column stream
     p.eager = (uint32_t)(eager >= 0 ? eager : tr ? 16 : 64);
     p.fail_count = fail_count;
     p.fail_rows = fail_rows;

@@ -26,6 +26,8 @@ MODES = {
     "default": {},
     "fallback_most_rows": {"SG_KNN_ALPHA": "5", "SG_KNN_BETA": "1"},
     "plain_rank_L": {"SG_KNN_ALPHA": "0"},
+    "cta_pair": {"SG_KNN_2CTA": "1"},                       # opt-in cta_group::2 kernel (knn_tc2.cu)
+    "cta_pair_fallback": {"SG_KNN_2CTA": "1", "SG_KNN_ALPHA": "5", "SG_KNN_BETA": "1"},
 }
 
 
