@@ -39,6 +39,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C1", choices=["C1", "C2", "C3", "C4"],
+                    help="C1: BASELINE configs[1] weak-scaled (1M x 128 and 4 shards per GPU, the driver's line); "
+                         "C2/C3/C4: the fixed 8-shard workloads of SURVEY 8(d) on any number of GPUs")
     ap.add_argument("--n-per-gpu", type=int, default=1_000_000)
     ap.add_argument("--shards-per-gpu", type=int, default=4)
     ap.add_argument("--no-e2e", action="store_true")
@@ -261,6 +264,15 @@ def emit(line: dict):
     os.write(fd, (json.dumps(line) + "\n").encode())
 
 
+CONFIGS = {
+    # name: (kind, n or None = n_per_gpu * world, d, shards or None = shards_per_gpu * world, scaling)
+    "C1": ("sift", None, 128, None, "weak"),
+    "C2": ("deep", 10_000_000, 96, 8, "strong"),
+    "C3": ("text", 5_000_000, 768, 8, "strong"),
+    "C4": ("sift_u8", 100_000_000, 128, 8, "strong"),
+}
+
+
 def main():
     global _OUT_FD
     args = parse()
@@ -273,7 +285,7 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2605_10135_b200 import api, datagen
-    from paper_2605_10135_b200.pipeline import BuildConfig, build_index, distribute_dataset, owned_rows
+    from paper_2605_10135_b200.pipeline import BuildConfig, build_index, gather_merged, make_comm
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -282,28 +294,33 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     api.load()
+    comm = make_comm(rank, world)   # the library's NCCL communicator: N1 + N2 of the path
     if args.profile_steps:
         args.no_e2e = args.no_cpu_baseline = args.no_recall = True
 
-    n = args.n_per_gpu * world
-    k = args.shards_per_gpu * world
+    kind, n_fix, d, k_fix, scaling = CONFIGS[args.config]
+    n = n_fix if n_fix else args.n_per_gpu * world
+    k = k_fix if k_fix else args.shards_per_gpu * world
+    if args.config != "C1":   # big workloads: evaluation legs off unless asked
+        args.no_cpu_baseline = True
     cfg = BuildConfig(k=k, omega=2, L=128, R=64)
-    x = datagen.sift_like(n, 128, device="cuda")
+    x = datagen._make(kind, n, d, datagen.DATA_SEED, "cuda")
     torch.cuda.synchronize()
+    elem = x.element_size()
 
     def barrier():
         if world > 1:
             dist.barrier()
 
     def step(inp):
-        return build_index(inp, cfg, rank, world)
+        return build_index(inp, cfg, rank, world, comm)
 
     for _ in range(args.warmup):
         idx = step(x)
     torch.cuda.synchronize()
     barrier()
 
-    # ---------------- timed region: inputs resident in HBM (512 MB > 126 MB L2 per rank)
+    # ---------------- timed region: inputs resident in HBM (larger than the 126 MB L2 per rank)
     api.scalegann_stats_read(reset=True)
     api.scalegann_stats_enable(True)
     clk = ClockSampler(local)
@@ -328,16 +345,16 @@ def main():
         ms = float(tt.item())
     value = n * args.steps / (ms / 1000.0)
 
-    # ---------------- roofline of the dominant kernel (distance tiles, tcgen05 kind::f16)
+    # ---------------- roofline of the dominant kernel (distance tiles, tcgen05)
     owned = [s for s in range(k) if idx.owner[s] == rank]
-    alg_flops_step = sum(2.0 * idx.sizes[s] ** 2 * 128 for s in owned)
+    alg_flops_step = sum(2.0 * idx.sizes[s] ** 2 * d for s in owned)
     peaks, src = load_peaks()
-    prec_is_f16 = True   # SIFT-shaped integer data -> F16_EXACT (AUTO)
+    prec_is_f16 = kind in ("sift", "sift_u8")   # integer data -> F16_EXACT (AUTO); float -> TF32 at half rate
     peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")) * (1.0 if prec_is_f16 else 0.5)
     achieved = alg_flops_step * args.steps / (knn_ms / 1000.0) / 1e12 if knn_ms > 0 else None
     traffic, pipe_pct, prof_src = None, None, None
     tp = os.path.join(ROOT, "profiles", "knn_dram_bytes.json")
-    if os.path.exists(tp):
+    if os.path.exists(tp) and args.config == "C1":
         try:
             prof = json.load(open(tp))
             traffic = prof.get("dram_bytes_per_launch")
@@ -348,64 +365,63 @@ def main():
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "ncu_tensor_pipe_active_pct": pipe_pct, "ncu_source": prof_src,
-                "kernel": "knn_tc_kernel (tcgen05.mma kind::f16, fp32 accumulate)",
-                "peak_source": f"{src} bf16 dense sustained (f16 = bf16 rate)",
-                "per_unit": "2*d flops per (row, column) pair; m_s^2 pairs per shard launch",
+                "kernel": "knn_tc_kernel (tcgen05.mma kind::%s, fp32 accumulate)" % ("f16" if prec_is_f16 else "tf32"),
+                "peak_source": f"{src} bf16 dense sustained" + (" (f16 = bf16 rate)" if prec_is_f16 else " x 0.5 (tf32)"),
+                "per_unit": f"2*d flops per (row, column) pair; m_s^2 pairs per shard launch (d = {d})",
                 "knn_ms_per_step": knn_ms / args.steps, "knn_launches": knn_launches,
                 "knn_share_of_step": (knn_ms / args.steps) / (ms / args.steps)}
 
     # ---------------- e2e through the public API with host buffers
     e2e = None
     if not args.no_e2e:
-        # this rank's slice crosses PCIe, the rest arrives over NVLink (pipeline.distribute_dataset);
-        # the merged rows this rank owns are read back
-        rows = n // world
-        xh = x[rank * rows:(rank + 1) * rows].cpu().pin_memory()
-        h2d = xh.numel() * xh.element_size()
-        # the owned rows (same partition every step) and a pinned host buffer, set up before timing
-        own = None if world == 1 else owned_rows(idx, rank)
-        shape = tuple(idx.merged.shape) if own is None else (int(own.sum().item()), idx.merged.shape[1])
-        outh = torch.empty(shape, dtype=idx.merged.dtype, pin_memory=True)
-        d2h = outh.numel() * outh.element_size()
+        # every rank copies the whole dataset host -> device (the partition runs on every rank,
+        # no dataset collective) and reads back the merged rows it owns
+        xh = x.cpu().pin_memory()
+        outh = torch.empty(tuple(idx.merged.shape), dtype=idx.merged.dtype, pin_memory=True)
+        h2d = xh.numel() * elem * world
+        d2h_local = outh.numel() * outh.element_size()
         barrier()
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(args.steps):
-            xd = distribute_dataset(xh.to("cuda", non_blocking=True), n, rank, world)
+            xd = xh.to("cuda", non_blocking=True)
             ix = step(xd)
-            outh.copy_(ix.merged if own is None else ix.merged[own], non_blocking=True)
+            outh.copy_(ix.merged, non_blocking=True)
         e1.record()
         torch.cuda.synchronize()
         barrier()
         ems = e0.elapsed_time(e1)
+        d2h = d2h_local
         if world > 1:
-            tt = torch.tensor([ems], dtype=torch.float64, device="cuda")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            ems = float(tt.item())
+            tt = torch.tensor([ems, float(d2h_local)], dtype=torch.float64, device="cuda")
+            t_max = tt.clone()
+            dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+            dist.all_reduce(tt, op=dist.ReduceOp.SUM)
+            ems, d2h = float(t_max[0].item()), int(tt[1].item())
         e2e = {"value": n * args.steps / (ems / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": ems / args.steps}
+               "d2h_bytes_per_step": d2h, "ms_per_step": ems / args.steps,
+               "note": "whole-job bytes: the full dataset to every rank, each rank's owned merged rows back"}
         del xh
 
     # ---------------- per-stage breakdown from one extra (untimed) step
-    stage_ms = build_index(x, cfg, rank, world, timing=True).stage_ms
+    stage_ms = build_index(x, cfg, rank, world, comm, timing=True).stage_ms
 
     # ---------------- recall@10 of the merged graph (untimed evaluation, a9)
     recall = None
     if not args.no_recall:
-        merged = idx.merged.clone()
-        if world > 1:
-            dist.all_reduce(merged, op=dist.ReduceOp.MAX)   # non-owned rows are -1
+        full = gather_merged(idx, rank, world)
         if rank == 0:
-            q = datagen.sift_like(10_000, 128, seed=datagen.DATA_SEED + datagen.QUERY_SEED_OFFSET, device="cuda")
+            q = datagen._make(kind, 10_000, d, datagen.DATA_SEED + datagen.QUERY_SEED_OFFSET, "cuda")
             recall = {}
             gt = None
             for beam in (32, 64, 128):
-                _, gt, r = api.scalegann_search_eval(x, merged, idx.entry, q, topk=10, beam=beam, gt=gt)
+                _, gt, r = api.scalegann_search_eval(x, full, idx.entry, q, topk=10, beam=beam, gt=gt)
                 recall[f"beam{beam}"] = r
+        del full
 
-    # ---------------- CPU oracle baseline (rank 0, N=1 only, bounded sample)
+    # ---------------- CPU oracle baseline + parity at bench size (rank 0, N=1 only)
     cpu = None
     parity = None
     if not args.no_cpu_baseline and world == 1 and rank == 0:
@@ -419,16 +435,20 @@ def main():
             parity = scale_parity(x, idx, cfg)
 
     if rank == 0:
+        wl = {"C1": f"C1 SIFT-shaped {n}x128 f32 integer-valued (weak: {n // world} per GPU)",
+              "C2": f"C2 DEEP-shaped {n}x96 f32 L2-normalised, {k} shards on {world} GPU(s)",
+              "C3": f"C3 text-embedding-shaped {n}x768 f32, {k} shards on {world} GPU(s)",
+              "C4": f"C4 BIGANN-shaped {n}x128 u8, {k} shards on {world} GPU(s)"}[args.config]
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f16", "data": "synthetic",
-            "config": {"workload": f"C1 SIFT-shaped {n}x128 f32 integer-valued (weak: {args.n_per_gpu} per GPU)",
-                       "n": n, "d": 128, "k": k, "omega": 2, "epsilon": 1.2, "L": 128, "R": 64,
-                       "precision": "F16_EXACT operands, fp32 accumulate (exact for this data)",
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": scaling,
+            "vs_baseline": None, "dtype": "f16" if prec_is_f16 else "tf32", "data": "synthetic",
+            "config": {"workload": wl, "n": n, "d": d, "k": k, "omega": 2, "epsilon": 1.2, "L": 128, "R": 64,
+                       "precision": ("F16_EXACT operands, fp32 accumulate (exact for this integer data)"
+                                     if prec_is_f16 else "TF32 operands (AUTO), fp32 accumulate"),
                        "shard_sizes": idx.sizes, "replicas": sum(idx.counts["repl"]),
-                       "l2": "inputs (512 MB/rank) larger than the 126 MB L2; no explicit flush",
-                       "parallelism": f"shard-parallel x{world} (LPT on m^2), NCCL bcast + all-to-all"},
+                       "l2": f"inputs ({n * d * elem / 1e6:.0f} MB/rank) larger than the 126 MB L2; no explicit flush",
+                       "parallelism": f"shard-parallel x{world} (LPT on m^2), library NCCL bcast + send/recv"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks, "recall_at_10": recall,
             "parity_at_scale": parity,
@@ -437,6 +457,7 @@ def main():
         emit(line)
     if world > 1:
         dist.barrier()
+        api.scalegann_comm_destroy(comm)
         dist.destroy_process_group()
 
 

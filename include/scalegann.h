@@ -46,7 +46,8 @@ typedef enum {
     SG_ERR_CUDA = 3,
     SG_ERR_CAPACITY = 4,    /* a primary found every cluster full */
     SG_ERR_WORKSPACE = 5,   /* ws_bytes smaller than the *_workspace() answer */
-    SG_ERR_TOO_SMALL = 6    /* shard with m < 2 */
+    SG_ERR_TOO_SMALL = 6,   /* shard with m < 2 */
+    SG_ERR_NCCL = 7         /* a collective failed (NCCL) */
 } sg_status;
 
 typedef enum { SG_U8 = 0, SG_F32 = 1 } sg_dtype;
@@ -180,42 +181,72 @@ sg_status scalegann_optimize_from_knn(const uint32_t* knn_ids, const float* knn_
                                       const sg_build_params* p, uint32_t* graph, float* graph_d,
                                       void* ws, size_t ws_bytes, void* stream);
 
-/* ---- a8: cross-shard merge by edge union + re-prune (R12) ----
- * Distributed protocol (one rank per GPU; shard s built on rank owner[s]):
- *   1. scalegann_merge_counts: per destination rank, how many replica rows
- *      this rank sends and receives (both computable locally from home[]).
- *   2. scalegann_merge_pack: record per (g, h>=1) with shard home[g][h] owned
- *      here, sent to owner[home[g][0]]: words [g, h, R global ids, R dist bits];
- *      records grouped by destination, ascending (g, h) within one.
- *   3. the caller exchanges the records (NCCL all-to-all over NVLink).
- *   4. scalegann_merge_union: for each g whose primary shard is owned here,
- *      union of the primary row and the received rows, dedupe by gid keeping
- *      the minimum distance, sort by (dist, gid), first R -> merged[g] (rows of
- *      n x R, only those owned here are written).
- * idmaps/graphs/graphs_d: HOST arrays of k DEVICE pointers (NULL for shards
- * not built here).  inv: n x omega local ids (scalegann_shard_idmap).  owner_host: k ranks.
- * Record size in uint32 words = 2 + 2R. */
-sg_status scalegann_merge_counts(const uint32_t* home, uint64_t n, uint32_t omega, uint32_t k,
-                                 const int32_t* owner_host, int rank, int world,
-                                 uint64_t* send_host, uint64_t* recv_host, void* ws, size_t ws_bytes,
-                                 void* stream);
-sg_status scalegann_merge_workspace(uint64_t n, uint32_t omega, uint32_t k, int world, size_t* bytes);
-sg_status scalegann_merge_pack(const uint32_t* home, const uint32_t* inv, uint64_t n, uint32_t omega,
-                               uint32_t k, const int32_t* owner_host, int rank, int world,
-                               const uint32_t* const* idmaps, const uint32_t* const* graphs,
-                               const float* const* graphs_d, uint32_t R, uint32_t* sendbuf,
-                               void* ws, size_t ws_bytes, void* stream);
-sg_status scalegann_merge_union(const uint32_t* home, const uint32_t* inv, uint64_t n, uint32_t omega,
-                                uint32_t k, const int32_t* owner_host, int rank,
-                                const uint32_t* const* idmaps, const uint32_t* const* graphs,
-                                const float* const* graphs_d, uint32_t R, const uint32_t* recvbuf,
-                                uint64_t n_recv, uint32_t* merged, float* merged_d, void* ws,
-                                size_t ws_bytes, void* stream);
-/* single-process merge of all k shards (owner = 0 for every shard) */
-sg_status scalegann_merge(const uint32_t* home, const uint32_t* inv, uint64_t n, uint32_t omega,
-                          uint32_t k, const uint32_t* const* idmaps, const uint32_t* const* graphs,
+/* ---- N1 / N2: the library's NCCL communicator ----------
+ * One rank per GPU.  Rank 0 creates a 128-byte unique id, the caller shares it with every rank
+ * out of band (file, MPI, torch.distributed, ...), and every rank calls scalegann_comm_init on
+ * its own device.  comm == NULL everywhere below means world = 1.  The communicator is the only
+ * resource the library owns; scalegann_comm_destroy releases it.  NCCL failures return
+ * SG_ERR_NCCL. */
+sg_status scalegann_get_unique_id(uint8_t out[128]);
+sg_status scalegann_comm_init(int rank, int world, const uint8_t uid[128], void** comm);
+sg_status scalegann_comm_destroy(void* comm);
+sg_status scalegann_comm_rank(void* comm, int* rank, int* world);
+/* N1: rank 0's k x d float32 centroids (device) to every rank, in place (ncclBroadcast). */
+sg_status scalegann_broadcast_centroids(void* comm, float* centroids, uint32_t k, uint32_t d, void* stream);
+/* N2: per-peer ncclSend/ncclRecv of merge records (`words` uint32 each) in one NCCL group.
+ * sendbuf holds this rank's records grouped by destination rank in rank order (send_host[r]
+ * records for rank r; those for this rank are skipped); recvbuf receives recv_host[r] records
+ * from each rank r, grouped by source in rank order. */
+sg_status scalegann_exchange_records(void* comm, const uint32_t* sendbuf, const uint64_t* send_host,
+                                     uint32_t* recvbuf, const uint64_t* recv_host, uint32_t words, void* stream);
+
+/* ---- a8: cross-shard merge by edge union + re-prune (R12) --------------------
+ * The merged row of a global vector g is kept by the rank that owns g's primary shard
+ * (home[g][0]): merged / merged_d hold n_owned x R rows of these g in ascending order
+ * (owned_index[g] = its row, SENTINEL for rows owned elsewhere).  Rows of vectors with one home
+ * are the shard row mapped to global ids as is; rows of vectors with several homes are the
+ * first R of the union of the homes' rows by (dist, gid), deduplicated by gid keeping the
+ * minimum carried distance, padded with (SENTINEL, +inf).  Bit-exact with the oracle.
+ *
+ * Streaming protocol (a shard's graph can be freed as soon as it has been merged):
+ *   1. scalegann_merge_plan: owned_index (n), send slots rec_slot (n x omega), per-rank record
+ *      counts send_host / recv_host (world each) and n_owned_host; synchronises;
+ *   2. scalegann_merge_init: merged rows to (SENTINEL, +inf);
+ *   3. scalegann_merge_shard for every shard built on this rank (graph: m x R local ids, idmap:
+ *      the shard's ascending global ids): rows whose primary is owned here are folded into
+ *      merged; the others become records [g, h, R global ids, R dist bits] in sendbuf
+ *      (2 + 2R uint32 each), grouped by destination rank, ascending g within a destination;
+ *   4. scalegann_exchange_records (N2);
+ *   5. scalegann_merge_finish: the received records folded in (ws >= 256 bytes); synchronises.
+ * owner_host: k ranks (shard s built on rank owner_host[s]); all ranks use the same home.
+ * Limits: k <= 64, world <= 64, R <= 128, n < 2^32 - 1. */
+sg_status scalegann_merge_plan_workspace(uint64_t n, size_t* bytes);
+sg_status scalegann_merge_plan(const uint32_t* home, uint64_t n, uint32_t omega, uint32_t k,
+                               const int32_t* owner_host, int rank, int world, uint32_t* owned_index,
+                               uint32_t* rec_slot, uint64_t* send_host, uint64_t* recv_host,
+                               uint64_t* n_owned_host, void* ws, size_t ws_bytes, void* stream);
+sg_status scalegann_merge_init(uint64_t n_owned, uint32_t R, uint32_t* merged, float* merged_d, void* stream);
+sg_status scalegann_merge_shard(const uint32_t* home, uint64_t n, uint32_t omega, uint32_t k,
+                                const int32_t* owner_host, int rank, int world, uint32_t shard,
+                                const uint32_t* idmap, uint64_t m, const uint32_t* graph,
+                                const float* graph_d, uint32_t R, const uint32_t* owned_index,
+                                const uint32_t* rec_slot, uint32_t* merged, float* merged_d,
+                                uint32_t* sendbuf, void* stream);
+sg_status scalegann_merge_finish(uint32_t omega, uint32_t R, const uint32_t* owned_index,
+                                 const uint32_t* recvbuf, uint64_t n_recv, uint32_t* merged,
+                                 float* merged_d, void* ws, size_t ws_bytes, void* stream);
+/* Collective one-call merge of every shard built on this rank (all ranks call it; steps 1-5 in
+ * the library, N2 over the communicator).  idmaps / graphs / graphs_d: HOST arrays of k DEVICE
+ * pointers (NULL for shards built elsewhere); sizes_host: k shard sizes.  The workspace query
+ * counts the records (synchronises) and returns n_owned (the rows of merged). */
+sg_status scalegann_merge_workspace(const uint32_t* home, uint64_t n, uint32_t omega, uint32_t k,
+                                    const int32_t* owner_host, void* comm, uint32_t R, size_t* bytes,
+                                    uint64_t* n_owned_host, void* stream);
+sg_status scalegann_merge(void* comm, const uint32_t* home, uint64_t n, uint32_t omega, uint32_t k,
+                          const int32_t* owner_host, const uint32_t* const* idmaps,
+                          const uint64_t* sizes_host, const uint32_t* const* graphs,
                           const float* const* graphs_d, uint32_t R, uint32_t* merged, float* merged_d,
-                          void* ws, size_t ws_bytes, void* stream);
+                          uint64_t* n_owned_host, void* ws, size_t ws_bytes, void* stream);
 
 /* ---- a9: recall evaluation (reading R14) ------------------
  * Greedy best-first beam search from `entry` over graph (n x R global ids) for

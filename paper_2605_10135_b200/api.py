@@ -18,7 +18,7 @@ SG_U8, SG_F32 = 0, 1
 SG_L2, SG_IP = 0, 1
 PREC_AUTO, PREC_F16_EXACT, PREC_TF32, PREC_TF32X3 = 0, 1, 2, 3
 _STATUS = {0: "SG_OK", 1: "SG_ERR_INVALID_ARG", 2: "SG_ERR_UNSUPPORTED", 3: "SG_ERR_CUDA",
-           4: "SG_ERR_CAPACITY", 5: "SG_ERR_WORKSPACE", 6: "SG_ERR_TOO_SMALL"}
+           4: "SG_ERR_CAPACITY", 5: "SG_ERR_WORKSPACE", 6: "SG_ERR_TOO_SMALL", 7: "SG_ERR_NCCL"}
 
 
 class ScaleGannError(RuntimeError):
@@ -45,8 +45,10 @@ EXPORTS = [
     "scalegann_partition_workspace", "scalegann_partition", "scalegann_shard_idmap_workspace",
     "scalegann_shard_idmap", "scalegann_entry_points", "scalegann_knn_workspace", "scalegann_knn",
     "scalegann_prune", "scalegann_reverse_workspace", "scalegann_reverse", "scalegann_build_shard_workspace",
-    "scalegann_build_shard", "scalegann_optimize_from_knn", "scalegann_merge_counts", "scalegann_merge_workspace",
-    "scalegann_merge_pack", "scalegann_merge_union", "scalegann_merge", "scalegann_search_workspace",
+    "scalegann_build_shard", "scalegann_optimize_from_knn", "scalegann_get_unique_id", "scalegann_comm_init",
+    "scalegann_comm_destroy", "scalegann_comm_rank", "scalegann_broadcast_centroids", "scalegann_exchange_records",
+    "scalegann_merge_plan_workspace", "scalegann_merge_plan", "scalegann_merge_init", "scalegann_merge_shard",
+    "scalegann_merge_finish", "scalegann_merge_workspace", "scalegann_merge", "scalegann_search_workspace",
     "scalegann_search_eval", "scalegann_search_shards_workspace", "scalegann_search_eval_shards", "scalegann_gemm_probe", "scalegann_stats_enable", "scalegann_stats_read", "scalegann_knn_profile",
 ]
 
@@ -89,14 +91,22 @@ def load(build_if_missing: bool = True):
         "scalegann_build_shard_workspace": ([u64, u32, i32, P(BuildParams), psz], i32),
         "scalegann_build_shard": ([vp, i32, u64, u32, vp, u64, P(BuildParams), vp, vp, vp, vp, vp, sz, vp], i32),
         "scalegann_optimize_from_knn": ([vp, vp, u64, P(BuildParams), vp, vp, vp, sz, vp], i32),
-        "scalegann_merge_counts": ([vp, u64, u32, u32, P(i32), ctypes.c_int, ctypes.c_int, pu64, pu64, vp, sz, vp],
-                                   i32),
-        "scalegann_merge_workspace": ([u64, u32, u32, ctypes.c_int, psz], i32),
-        "scalegann_merge_pack": ([vp, vp, u64, u32, u32, P(i32), ctypes.c_int, ctypes.c_int, P(vp), P(vp), P(vp), u32,
-                                  vp, vp, sz, vp], i32),
-        "scalegann_merge_union": ([vp, vp, u64, u32, u32, P(i32), ctypes.c_int, P(vp), P(vp), P(vp), u32, vp, u64, vp,
-                                   vp, vp, sz, vp], i32),
-        "scalegann_merge": ([vp, vp, u64, u32, u32, P(vp), P(vp), P(vp), u32, vp, vp, vp, sz, vp], i32),
+        "scalegann_get_unique_id": ([ctypes.c_char_p], i32),
+        "scalegann_comm_init": ([ctypes.c_int, ctypes.c_int, ctypes.c_char_p, P(vp)], i32),
+        "scalegann_comm_destroy": ([vp], i32),
+        "scalegann_comm_rank": ([vp, P(ctypes.c_int), P(ctypes.c_int)], i32),
+        "scalegann_broadcast_centroids": ([vp, vp, u32, u32, vp], i32),
+        "scalegann_exchange_records": ([vp, vp, pu64, vp, pu64, u32, vp], i32),
+        "scalegann_merge_plan_workspace": ([u64, psz], i32),
+        "scalegann_merge_plan": ([vp, u64, u32, u32, P(i32), ctypes.c_int, ctypes.c_int, vp, vp, pu64, pu64, pu64, vp,
+                                  sz, vp], i32),
+        "scalegann_merge_init": ([u64, u32, vp, vp, vp], i32),
+        "scalegann_merge_shard": ([vp, u64, u32, u32, P(i32), ctypes.c_int, ctypes.c_int, u32, vp, u64, vp, vp, u32,
+                                   vp, vp, vp, vp, vp, vp], i32),
+        "scalegann_merge_finish": ([u32, u32, vp, vp, u64, vp, vp, vp, sz, vp], i32),
+        "scalegann_merge_workspace": ([vp, u64, u32, u32, P(i32), vp, u32, psz, pu64, vp], i32),
+        "scalegann_merge": ([vp, vp, u64, u32, u32, P(i32), P(vp), pu64, P(vp), P(vp), u32, vp, vp, pu64, vp, sz,
+                             vp], i32),
         "scalegann_search_workspace": ([u64, u32, i32, u32, u32, u32, psz], i32),
         "scalegann_search_eval": ([vp, i32, u64, u32, vp, u32, u32, vp, u32, u32, u32, i32, vp, vp, vp,
                                    P(ctypes.c_double), vp, sz, vp], i32),
@@ -337,63 +347,114 @@ def _ptr_array(ts, k):
     return arr
 
 
-def scalegann_merge_counts(home, k, owner, rank, world, ws=None):
+# ----------------------------------------------------------------------------- N1 / N2 communicator
+def scalegann_get_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(load().scalegann_get_unique_id(buf))
+    return buf.raw
+
+
+def scalegann_comm_init(rank: int, world: int, uid: bytes):
+    """The library's NCCL communicator on the current device (opaque handle)."""
+    assert len(uid) == 128
+    c = ctypes.c_void_p()
+    _check(load().scalegann_comm_init(rank, world, uid, ctypes.byref(c)))
+    return c
+
+
+def scalegann_comm_destroy(comm):
+    if comm is not None:
+        _check(load().scalegann_comm_destroy(comm))
+
+
+def scalegann_comm_rank(comm):
+    r, w = ctypes.c_int(0), ctypes.c_int(0)
+    _check(load().scalegann_comm_rank(comm, ctypes.byref(r), ctypes.byref(w)))
+    return r.value, w.value
+
+
+def scalegann_broadcast_centroids(comm, centroids):
+    """N1: rank 0's centroids to every rank, in place."""
+    _dev(centroids, "centroids")
+    k, d = centroids.shape
+    _check(load().scalegann_broadcast_centroids(comm, _ptr(centroids), k, d, _stream()))
+    return centroids
+
+
+def scalegann_exchange_records(comm, sendbuf, send, recv, words):
+    """N2: per-peer send/recv of merge records; returns the receive buffer (int32 view)."""
+    nrecv = sum(recv)
+    recvbuf = torch.empty(max(nrecv, 1) * words, dtype=torch.int32, device=sendbuf.device)
+    world = len(send)
+    _check(load().scalegann_exchange_records(comm, _ptr(sendbuf), (ctypes.c_uint64 * world)(*send), _ptr(recvbuf),
+                                             (ctypes.c_uint64 * world)(*recv), words, _stream()))
+    return recvbuf
+
+
+# ----------------------------------------------------------------------------- a8
+def scalegann_merge_plan(home, owner, rank, world, ws=None):
+    """Returns (owned_index n int32 [uint32 bits], rec_slot n x omega, send list, recv list, n_owned)."""
     L = load()
+    _dev(home, "home")
     n, omega = home.shape
-    own = (ctypes.c_int32 * k)(*owner)
+    k = len(owner)
+    owned_index = torch.empty(n, dtype=torch.int32, device=home.device)
+    rec_slot = torch.empty(n, omega, dtype=torch.int32, device=home.device)
     send = (ctypes.c_uint64 * world)()
     recv = (ctypes.c_uint64 * world)()
-    nb = _size_q(L.scalegann_merge_workspace, n, omega, k, world)
+    no = ctypes.c_uint64(0)
+    nb = _size_q(L.scalegann_merge_plan_workspace, n)
     p, nbytes = _ws(nb, ws)
-    _check(L.scalegann_merge_counts(_ptr(home), n, omega, k, own, rank, world, send, recv, p, nbytes, _stream()))
-    return list(send), list(recv)
+    _check(L.scalegann_merge_plan(_ptr(home), n, omega, k, (ctypes.c_int32 * k)(*owner), rank, world, _ptr(owned_index),
+                                  _ptr(rec_slot), send, recv, ctypes.byref(no), p, nbytes, _stream()))
+    return owned_index, rec_slot, list(send), list(recv), no.value
 
 
-def scalegann_merge_pack(home, inv, owner, rank, world, idmaps, graphs, graphs_d, n_send, ws=None):
-    L = load()
-    n, omega = home.shape
-    k = len(owner)
-    R = next(g for g in graphs if g is not None).shape[1]
-    W = 2 + 2 * R
-    sendbuf = torch.empty(max(n_send, 1) * W, dtype=torch.int32, device=home.device)
-    nb = _size_q(L.scalegann_merge_workspace, n, omega, k, world)
-    p, nbytes = _ws(nb, ws)
-    _check(L.scalegann_merge_pack(_ptr(home), _ptr(inv), n, omega, k, (ctypes.c_int32 * k)(*owner), rank, world,
-                                  _ptr_array(idmaps, k), _ptr_array(graphs, k), _ptr_array(graphs_d, k), R,
-                                  _ptr(sendbuf), p, nbytes, _stream()))
-    return sendbuf[: n_send * W]
-
-
-def scalegann_merge_union(home, inv, owner, rank, idmaps, graphs, graphs_d, recvbuf, n_recv, merged=None,
-                          merged_d=None, ws=None):
-    L = load()
-    n, omega = home.shape
-    k = len(owner)
-    R = next(g for g in graphs if g is not None).shape[1]
-    if merged is None:
-        merged = torch.full((n, R), -1, dtype=torch.int32, device=home.device)
-        merged_d = torch.full((n, R), float("inf"), dtype=torch.float32, device=home.device)
-    nb = _size_q(L.scalegann_merge_workspace, n, omega, k, 1)
-    p, nbytes = _ws(nb, ws)
-    _check(L.scalegann_merge_union(_ptr(home), _ptr(inv), n, omega, k, (ctypes.c_int32 * k)(*owner), rank,
-                                   _ptr_array(idmaps, k), _ptr_array(graphs, k), _ptr_array(graphs_d, k), R,
-                                   _ptr(recvbuf), n_recv, _ptr(merged), _ptr(merged_d), p, nbytes, _stream()))
+def scalegann_merge_init(n_owned, R, device="cuda"):
+    merged = torch.empty(max(n_owned, 1), R, dtype=torch.int32, device=device)[:n_owned]
+    merged_d = torch.empty(max(n_owned, 1), R, dtype=torch.float32, device=device)[:n_owned]
+    _check(load().scalegann_merge_init(n_owned, R, _ptr(merged), _ptr(merged_d), _stream()))
     return merged, merged_d
 
 
-def scalegann_merge(home, inv, idmaps, graphs, graphs_d, ws=None):
-    """Single-process merge of all k shards."""
+def scalegann_merge_shard(home, owner, rank, world, shard, idmap, graph, graph_d, owned_index, rec_slot, merged,
+                          merged_d, sendbuf):
+    n, omega = home.shape
+    k = len(owner)
+    m, R = graph.shape
+    _check(load().scalegann_merge_shard(_ptr(home), n, omega, k, (ctypes.c_int32 * k)(*owner), rank, world, shard,
+                                        _ptr(idmap), m, _ptr(graph), _ptr(graph_d), R, _ptr(owned_index),
+                                        _ptr(rec_slot), _ptr(merged), _ptr(merged_d), _ptr(sendbuf), _stream()))
+
+
+def scalegann_merge_finish(omega, owned_index, recvbuf, n_recv, merged, merged_d, ws=None):
+    R = merged.shape[1]
+    p, nbytes = _ws(4096, ws)
+    _check(load().scalegann_merge_finish(omega, R, _ptr(owned_index), _ptr(recvbuf), n_recv, _ptr(merged),
+                                         _ptr(merged_d), p, nbytes, _stream()))
+
+
+def scalegann_merge(home, idmaps, graphs, graphs_d, owner=None, comm=None, ws=None):
+    """One-call collective merge of the shards built on this rank (graphs[s] None elsewhere).
+    Returns (merged, merged_d): the rows of the globals whose primary shard is owned here, in
+    ascending global id (all n rows at world 1)."""
     L = load()
     n, omega = home.shape
     k = len(idmaps)
-    R = graphs[0].shape[1]
-    merged = torch.empty(n, R, dtype=torch.int32, device=home.device)
-    merged_d = torch.empty(n, R, dtype=torch.float32, device=home.device)
-    nrec = int((home[:, 1:] != -1).sum().item()) if omega > 1 else 0
-    nb = _size_q(L.scalegann_merge_workspace, n, omega, k, 1) + nrec * (2 + 2 * R) * 4 + 4096
-    p, nbytes = _ws(nb, ws)
-    _check(L.scalegann_merge(_ptr(home), _ptr(inv), n, omega, k, _ptr_array(idmaps, k), _ptr_array(graphs, k),
-                             _ptr_array(graphs_d, k), R, _ptr(merged), _ptr(merged_d), p, nbytes, _stream()))
+    owner = [0] * k if owner is None else owner
+    R = next(g for g in graphs if g is not None).shape[1]
+    own = (ctypes.c_int32 * k)(*owner)
+    nbytes_q = ctypes.c_size_t(0)
+    no = ctypes.c_uint64(0)
+    _check(L.scalegann_merge_workspace(_ptr(home), n, omega, k, own, comm, R, ctypes.byref(nbytes_q),
+                                       ctypes.byref(no), _stream()))
+    merged = torch.empty(max(no.value, 1), R, dtype=torch.int32, device=home.device)[:no.value]
+    merged_d = torch.empty(max(no.value, 1), R, dtype=torch.float32, device=home.device)[:no.value]
+    sizes = (ctypes.c_uint64 * k)(*[0 if a is None else a.numel() for a in idmaps])
+    p, nbytes = _ws(nbytes_q.value, ws)
+    _check(L.scalegann_merge(comm, _ptr(home), n, omega, k, own, _ptr_array(idmaps, k), sizes, _ptr_array(graphs, k),
+                             _ptr_array(graphs_d, k), R, _ptr(merged), _ptr(merged_d), ctypes.byref(no), p, nbytes,
+                             _stream()))
     return merged, merged_d
 
 

@@ -11,12 +11,31 @@ CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build", os.environ.get("SG_OBJ_DIR", "obj"))
 LIB = os.environ.get("SG_LIB_PATH", os.path.join(HERE, "libscalegann.so"))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+
+def _nccl_dir() -> str:
+    """The NCCL that torch loads (the nvidia-nccl wheel), so one NCCL serves the whole process;
+    the system NCCL otherwise."""
+    try:
+        import nvidia.nccl as _n
+        d = list(_n.__path__)[0]
+        if os.path.exists(os.path.join(d, "include", "nccl.h")):
+            return d
+    except Exception:
+        pass
+    return ""
+
+
+NCCL = _nccl_dir()
+NCCL_INC = ["-I", os.path.join(NCCL, "include")] if NCCL else []
+NCCL_LINK = (["-Xlinker", os.path.join(NCCL, "lib", "libnccl.so.2"), "-Xlinker", "-rpath=" + os.path.join(NCCL, "lib")]
+             if NCCL else ["-lnccl"])
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
     "-Xcompiler", "-fPIC",
     "-I", os.path.join(os.path.dirname(HERE), "include"),
-] + os.environ.get("SG_NVCC_FLAGS", "").split()
+] + NCCL_INC + os.environ.get("SG_NVCC_FLAGS", "").split()
 
 
 def _deps_mtime() -> float:
@@ -51,7 +70,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         objs = list(ex.map(lambda s: _compile(s, verbose), srcs))
     tmp = LIB + ".tmp"
-    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs]
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs, *NCCL_LINK]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")

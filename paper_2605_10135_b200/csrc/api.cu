@@ -24,18 +24,20 @@ sg_status entry_run(const uint32_t* home, const float* pd, uint64_t n, uint32_t 
                     const uint64_t* sizes_host, uint32_t* entry_host, uint32_t* global_host, void* ws,
                     size_t ws_bytes, cudaStream_t st);
 size_t reverse_ws(uint64_t m, uint32_t R);
-sg_status merge_counts_run(const uint32_t* home, uint64_t n, uint32_t omega, uint32_t k, const int32_t* owner,
-                           int rank, int world, uint64_t* send_host, uint64_t* recv_host, void* ws, size_t ws_bytes,
-                           cudaStream_t st);
-size_t merge_ws(uint64_t n, uint32_t omega);
-sg_status merge_pack_run(const uint32_t* home, const uint32_t* inv, uint64_t n, uint32_t omega, uint32_t k,
-                         const int32_t* owner, int rank, int world, const uint32_t* const* idmaps,
-                         const uint32_t* const* graphs, const float* const* graphs_d, uint32_t R, uint32_t* sendbuf,
-                         void* ws, size_t ws_bytes, cudaStream_t st);
-sg_status merge_union_run(const uint32_t* home, const uint32_t* inv, uint64_t n, uint32_t omega, uint32_t k,
-                          const int32_t* owner, int rank, const uint32_t* const* idmaps, const uint32_t* const* graphs,
-                          const float* const* graphs_d, uint32_t R, const uint32_t* recvbuf, uint64_t n_recv,
-                          uint32_t* merged, float* merged_d, void* ws, size_t ws_bytes, cudaStream_t st);
+size_t merge_plan_ws(uint64_t n);
+sg_status merge_plan_run(const uint32_t* home, uint64_t n, uint32_t omega, uint32_t k, const int32_t* owner, int rank,
+                         int world, uint32_t* owned_index, uint32_t* rec_slot, uint64_t* send_host, uint64_t* recv_host,
+                         uint64_t* n_owned_host, void* ws, size_t ws_bytes, cudaStream_t st);
+sg_status merge_init_run(uint64_t n_owned, uint32_t R, uint32_t* merged, float* merged_d, cudaStream_t st);
+sg_status merge_shard_run(const uint32_t* home, uint32_t omega, uint32_t k, const int32_t* owner, int rank, int world,
+                          uint32_t shard, const uint32_t* idmap, uint64_t m, const uint32_t* graph, const float* graph_d,
+                          uint32_t R, const uint32_t* owned_index, const uint32_t* rec_slot, uint32_t* merged,
+                          float* merged_d, uint32_t* sendbuf, cudaStream_t st);
+sg_status merge_finish_run(uint32_t omega, uint32_t R, const uint32_t* owned_index, const uint32_t* recvbuf,
+                           uint64_t n_recv, uint32_t* merged, float* merged_d, int* err_dev, cudaStream_t st);
+sg_status comm_rank_world(void* comm, int* rank, int* world);
+sg_status exchange_records_run(void* comm, const uint32_t* sendbuf, const uint64_t* send_host, uint32_t* recvbuf,
+                               const uint64_t* recv_host, uint32_t words, cudaStream_t st);
 size_t beam_ws(uint64_t n, uint32_t nq);
 sg_status beam_run(const void* x, sg_dtype dtype, uint64_t n, uint32_t d, const uint32_t* graph, uint32_t R,
                    uint32_t entry, const void* q, uint32_t nq, uint32_t topk, uint32_t beam, int metric,
@@ -372,52 +374,127 @@ sg_status scalegann_build_shard(const void* x, sg_dtype dtype, uint64_t n, uint3
 }
 
 // ------------------------------------------------------------------ a8
-sg_status scalegann_merge_counts(const uint32_t* home, uint64_t n, uint32_t omega, uint32_t k, const int32_t* owner_host,
-                                 int rank, int world, uint64_t* send_host, uint64_t* recv_host, void* ws,
-                                 size_t ws_bytes, void* stream) {
-    SG_CHECK_ARG(home && owner_host && omega >= 1, "merge_counts: bad arguments");
-    return merge_counts_run(home, n, omega, k, owner_host, rank, world, send_host, recv_host, ws, ws_bytes, S(stream));
-}
-sg_status scalegann_merge_workspace(uint64_t n, uint32_t omega, uint32_t k, int world, size_t* bytes) {
+sg_status scalegann_merge_plan_workspace(uint64_t n, size_t* bytes) {
     SG_CHECK_ARG(bytes, "null bytes");
-    (void)k; (void)world;
-    *bytes = merge_ws(n, omega);
+    *bytes = merge_plan_ws(n);
     return SG_OK;
 }
-sg_status scalegann_merge_pack(const uint32_t* home, const uint32_t* inv, uint64_t n, uint32_t omega, uint32_t k,
-                               const int32_t* owner_host, int rank, int world, const uint32_t* const* idmaps,
-                               const uint32_t* const* graphs, const float* const* graphs_d, uint32_t R,
-                               uint32_t* sendbuf, void* ws, size_t ws_bytes, void* stream) {
-    SG_CHECK_ARG(home && inv && owner_host && idmaps && graphs && graphs_d && R >= 1, "merge_pack: bad arguments");
-    return merge_pack_run(home, inv, n, omega, k, owner_host, rank, world, idmaps, graphs, graphs_d, R, sendbuf, ws,
-                          ws_bytes, S(stream));
+sg_status scalegann_merge_plan(const uint32_t* home, uint64_t n, uint32_t omega, uint32_t k, const int32_t* owner_host,
+                               int rank, int world, uint32_t* owned_index, uint32_t* rec_slot, uint64_t* send_host,
+                               uint64_t* recv_host, uint64_t* n_owned_host, void* ws, size_t ws_bytes, void* stream) {
+    SG_CHECK_ARG(home && owner_host && omega >= 1 && n > 0 && n < 0xFFFFFFFFull, "merge_plan: bad arguments");
+    return merge_plan_run(home, n, omega, k, owner_host, rank, world, owned_index, rec_slot, send_host, recv_host,
+                          n_owned_host, ws, ws_bytes, S(stream));
 }
-sg_status scalegann_merge_union(const uint32_t* home, const uint32_t* inv, uint64_t n, uint32_t omega, uint32_t k,
-                                const int32_t* owner_host, int rank, const uint32_t* const* idmaps,
-                                const uint32_t* const* graphs, const float* const* graphs_d, uint32_t R,
-                                const uint32_t* recvbuf, uint64_t n_recv, uint32_t* merged, float* merged_d, void* ws,
-                                size_t ws_bytes, void* stream) {
-    SG_CHECK_ARG(home && inv && owner_host && idmaps && graphs && graphs_d && merged && merged_d && R >= 1,
-                 "merge_union: bad arguments");
-    SG_CHECK_ARG(n_recv == 0 || recvbuf, "merge_union: null recvbuf");
-    return merge_union_run(home, inv, n, omega, k, owner_host, rank, idmaps, graphs, graphs_d, R, recvbuf, n_recv,
-                           merged, merged_d, ws, ws_bytes, S(stream));
+sg_status scalegann_merge_init(uint64_t n_owned, uint32_t R, uint32_t* merged, float* merged_d, void* stream) {
+    SG_CHECK_ARG((merged && merged_d) || n_owned == 0, "merge_init: null output");
+    SG_CHECK_ARG(R >= 1 && R <= 128, "merge_init: R must be in [1, 128]");
+    return merge_init_run(n_owned, R, merged, merged_d, S(stream));
 }
-sg_status scalegann_merge(const uint32_t* home, const uint32_t* inv, uint64_t n, uint32_t omega, uint32_t k,
-                          const uint32_t* const* idmaps, const uint32_t* const* graphs, const float* const* graphs_d,
-                          uint32_t R, uint32_t* merged, float* merged_d, void* ws, size_t ws_bytes, void* stream) {
-    SG_CHECK_ARG(k >= 1 && k <= 64, "merge: k must be in [1, 64]");
-    int32_t owner[64] = {0};
-    uint64_t send = 0;
-    SG_TRY(merge_counts_run(home, n, omega, k, owner, 0, 1, &send, nullptr, ws, ws_bytes, S(stream)));
-    // the record buffer sits after the merge scratch in the same workspace
-    const size_t mw = merge_ws(n, omega);
-    const size_t need = mw + send * (2 + 2 * (size_t)R) * 4 + 256;
+sg_status scalegann_merge_shard(const uint32_t* home, uint64_t n, uint32_t omega, uint32_t k, const int32_t* owner_host,
+                                int rank, int world, uint32_t shard, const uint32_t* idmap, uint64_t m,
+                                const uint32_t* graph, const float* graph_d, uint32_t R, const uint32_t* owned_index,
+                                const uint32_t* rec_slot, uint32_t* merged, float* merged_d, uint32_t* sendbuf,
+                                void* stream) {
+    SG_CHECK_ARG(home && owner_host && n > 0 && omega >= 1, "merge_shard: bad arguments");
+    SG_CHECK_ARG(m == 0 || (idmap && graph && graph_d && owned_index && rec_slot), "merge_shard: null pointer");
+    (void)n;
+    return merge_shard_run(home, omega, k, owner_host, rank, world, shard, idmap, m, graph, graph_d, R, owned_index,
+                           rec_slot, merged, merged_d, sendbuf, S(stream));
+}
+sg_status scalegann_merge_finish(uint32_t omega, uint32_t R, const uint32_t* owned_index, const uint32_t* recvbuf,
+                                 uint64_t n_recv, uint32_t* merged, float* merged_d, void* ws, size_t ws_bytes,
+                                 void* stream) {
+    SG_CHECK_ARG(n_recv == 0 || (recvbuf && owned_index && merged && merged_d), "merge_finish: null pointer");
+    Carver cv(ws, ws_bytes);
+    int* err = cv.take<int>(1);
+    if (!cv.ok() || !ws) { set_error("merge_finish: workspace too small"); return SG_ERR_WORKSPACE; }
+    return merge_finish_run(omega, R, owned_index, recvbuf, n_recv, merged, merged_d, err, S(stream));
+}
+
+// collective merge: workspace = owned index + send slots + plan scratch + both record buffers
+static sg_status merge_sizes(const uint32_t* home, uint64_t n, uint32_t omega, uint32_t k, const int32_t* owner_host,
+                             void* comm, uint32_t R, size_t* bytes, uint64_t* n_owned, uint64_t* send, uint64_t* recv,
+                             int* rank, int* world, void* ws, size_t ws_bytes, cudaStream_t st) {
+    SG_TRY(comm_rank_world(comm, rank, world));
+    const size_t pw = merge_plan_ws(n);
+    Carver cv(nullptr, 0);
+    cv.take<uint32_t>(n);           // owned_index
+    cv.take<uint32_t>(n * omega);   // send slots
+    cv.take<uint8_t>(pw);           // plan scratch
+    cv.take<int>(1);
+    const size_t fixed = cv.off + 4096;
+    if (!ws) {
+        // counting needs scratch of its own: the plan scratch alone, from a temporary buffer
+        void* tmp = nullptr;
+        SG_CUDA(cudaMallocAsync(&tmp, pw, st));
+        sg_status e = merge_plan_run(home, n, omega, k, owner_host, *rank, *world, nullptr, nullptr, send, recv, n_owned,
+                                     tmp, pw, st);
+        cudaFreeAsync(tmp, st);
+        SG_TRY(e);
+    } else {
+        if (ws_bytes < fixed) { set_error("merge: workspace too small"); return SG_ERR_WORKSPACE; }
+        SG_TRY(merge_plan_run(home, n, omega, k, owner_host, *rank, *world, nullptr, nullptr, send, recv, n_owned, ws,
+                              ws_bytes, st));
+    }
+    uint64_t ns = 0, nr = 0;
+    for (int r = 0; r < *world; r++) { ns += send[r]; nr += recv[r]; }
+    *bytes = fixed + (ns + nr) * (2 + 2 * (size_t)R) * 4 + 512;
+    return SG_OK;
+}
+
+sg_status scalegann_merge_workspace(const uint32_t* home, uint64_t n, uint32_t omega, uint32_t k,
+                                    const int32_t* owner_host, void* comm, uint32_t R, size_t* bytes,
+                                    uint64_t* n_owned_host, void* stream) {
+    SG_CHECK_ARG(home && owner_host && bytes && n > 0 && omega >= 1, "merge_workspace: bad arguments");
+    uint64_t send[64], recv[64], no = 0;
+    int rank, world;
+    SG_TRY(merge_sizes(home, n, omega, k, owner_host, comm, R, bytes, &no, send, recv, &rank, &world, nullptr, 0,
+                       S(stream)));
+    if (n_owned_host) *n_owned_host = no;
+    return SG_OK;
+}
+
+sg_status scalegann_merge(void* comm, const uint32_t* home, uint64_t n, uint32_t omega, uint32_t k,
+                          const int32_t* owner_host, const uint32_t* const* idmaps, const uint64_t* sizes_host,
+                          const uint32_t* const* graphs, const float* const* graphs_d, uint32_t R, uint32_t* merged,
+                          float* merged_d, uint64_t* n_owned_host, void* ws, size_t ws_bytes, void* stream) {
+    SG_CHECK_ARG(home && owner_host && idmaps && sizes_host && graphs && graphs_d && n > 0 && omega >= 1,
+                 "merge: bad arguments");
+    SG_CHECK_ARG(k >= 1 && k <= 64 && R >= 1 && R <= 128, "merge: need 1 <= k <= 64, 1 <= R <= 128");
+    cudaStream_t st = S(stream);
+    uint64_t send[64], recv[64], no = 0;
+    int rank, world;
+    size_t need = 0;
+    SG_TRY(merge_sizes(home, n, omega, k, owner_host, comm, R, &need, &no, send, recv, &rank, &world, ws, ws_bytes, st));
     if (ws_bytes < need) { set_error("merge: workspace too small (need %zu)", need); return SG_ERR_WORKSPACE; }
-    uint32_t* rec = (uint32_t*)((uint8_t*)ws + ((mw + 255) & ~(size_t)255));
-    SG_TRY(merge_pack_run(home, inv, n, omega, k, owner, 0, 1, idmaps, graphs, graphs_d, R, rec, ws, mw, S(stream)));
-    return merge_union_run(home, inv, n, omega, k, owner, 0, idmaps, graphs, graphs_d, R, rec, send, merged, merged_d,
-                           ws, mw, S(stream));
+    SG_CHECK_ARG(no == 0 || (merged && merged_d), "merge: null merged output");
+    for (uint32_t s = 0; s < k; s++)
+        SG_CHECK_ARG(owner_host[s] != rank || sizes_host[s] == 0 || (idmaps[s] && graphs[s] && graphs_d[s]),
+                     "merge: an owned shard has no graph");
+    Carver cv(ws, ws_bytes);
+    uint32_t* owned_index = cv.take<uint32_t>(n);
+    uint32_t* rec_slot = cv.take<uint32_t>(n * omega);
+    uint8_t* pws = cv.take<uint8_t>(merge_plan_ws(n));
+    int* err = cv.take<int>(1);
+    uint64_t ns = 0, nr = 0;
+    for (int r = 0; r < world; r++) { ns += send[r]; nr += recv[r]; }
+    const uint32_t W = 2 + 2 * R;
+    uint32_t* sendbuf = cv.take<uint32_t>(ns * W);
+    uint32_t* recvbuf = cv.take<uint32_t>(nr * W);
+    if (!cv.ok()) { set_error("merge: workspace too small"); return SG_ERR_WORKSPACE; }
+    SG_TRY(merge_plan_run(home, n, omega, k, owner_host, rank, world, owned_index, rec_slot, send, recv, &no, pws,
+                          merge_plan_ws(n), st));
+    SG_TRY(merge_init_run(no, R, merged, merged_d, st));
+    for (uint32_t s = 0; s < k; s++) {
+        if (owner_host[s] != rank || sizes_host[s] == 0) continue;
+        SG_TRY(merge_shard_run(home, omega, k, owner_host, rank, world, s, idmaps[s], sizes_host[s], graphs[s],
+                               graphs_d[s], R, owned_index, rec_slot, merged, merged_d, sendbuf, st));
+    }
+    SG_TRY(exchange_records_run(comm, sendbuf, send, recvbuf, recv, W, st));
+    SG_TRY(merge_finish_run(omega, R, owned_index, recvbuf, nr, merged, merged_d, err, st));
+    if (n_owned_host) *n_owned_host = no;
+    return SG_OK;
 }
 
 // ------------------------------------------------------------------ a9

@@ -1,14 +1,16 @@
 """One pass of the ScaleGANN hot path through the C ABI.
 
-    a1  centroids: scalegann_kmeans on rank 0, NCCL broadcast to every rank
+    a1  centroids: scalegann_kmeans on rank 0, N1 scalegann_broadcast_centroids
     a2-a3 partition: scalegann_partition, identical on every rank
-    a4-a7 per owned shard: scalegann_shard_idmap + scalegann_build_shard
-    a8  merge: scalegann_merge_pack -> NCCL all-to-all over NVLink -> scalegann_merge_union
-        (P:139); single process: scalegann_merge
+    a4-a7 per owned shard: scalegann_shard_idmap + scalegann_build_shard, each shard
+        folded into the merged rows (scalegann_merge_shard) and freed before the next one
+    a8  merge: N2 scalegann_exchange_records of the rows whose primary is owned elsewhere, then
+        scalegann_merge_finish
 
 Shard placement across ranks is LPT on m^2 (the exact kNN costs O(m^2) per shard); shards are
-independent builds ("no ... inter-GPU communication").  torch.distributed provides the
-process group; the only collectives are the centroid broadcast and the merge all-to-all.
+independent builds ("no ... inter-GPU communication").  Both collectives run on the
+library's own NCCL communicator (share_unique_id bootstraps it over torch.distributed); they
+are the only data exchanged between ranks.
 """
 from __future__ import annotations
 
@@ -43,7 +45,7 @@ class BuildConfig:
 
 @dataclasses.dataclass
 class Index:
-    merged: torch.Tensor          # n x R global ids (rows owned by this rank filled)
+    merged: torch.Tensor          # n_owned x R global ids: rows of the globals whose primary shard is owned here
     merged_d: torch.Tensor
     entry: int
     home: torch.Tensor
@@ -53,6 +55,7 @@ class Index:
     counts: dict
     owner: list
     stage_ms: dict
+    owned_index: torch.Tensor | None = None   # row of g in merged (SENT if owned elsewhere)
     launches: int = 0
 
 
@@ -68,34 +71,22 @@ def lpt_owner(sizes, world):
     return owner
 
 
-def broadcast_centroids(C: torch.Tensor, world: int) -> torch.Tensor:
-    """N1: rank 0's k x d centroids to every rank (in place; NCCL over NVLink on GPUs)."""
+def share_unique_id(rank: int, world: int) -> bytes:
+    """Rank 0's 128-byte NCCL unique id to every rank over the torch.distributed process group
+    (bootstrap only; works with gloo and nccl)."""
+    uid = api.scalegann_get_unique_id() if rank == 0 else bytes(128)
     if world > 1:
-        dist.broadcast(C, src=0)
-    return C
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    return uid
 
 
-def exchange_records(sendbuf: torch.Tensor, send: list, recv: list, W: int) -> torch.Tensor:
-    """N2: all-to-all of the merge records (W int32 words each).  `send[r]` / `recv[r]` count the
-    records this rank sends to / receives from rank r (both known locally from `home`, so no count
-    exchange is needed); records arrive grouped by source rank, in rank order."""
-    nrecv = sum(recv)
-    recvbuf = torch.empty(max(nrecv, 1) * W, dtype=torch.int32, device=sendbuf.device)
-    dist.all_to_all_single(recvbuf[: nrecv * W], sendbuf[: sum(send) * W], [c * W for c in recv],
-                           [c * W for c in send])
-    return recvbuf
-
-
-def distribute_dataset(x_local: torch.Tensor, n: int, rank: int, world: int) -> torch.Tensor:
-    """Every rank holds the full dataset (the partition runs identically everywhere),
-    but only its contiguous 1/world slice crosses PCIe: the slices are all-gathered over NVLink.
-    `x_local` is this rank's rows [rank*n/world, (rank+1)*n/world) on the device."""
+def make_comm(rank: int, world: int):
+    """The library communicator for this rank (None at world 1)."""
     if world == 1:
-        return x_local
-    assert n % world == 0, "n must be a multiple of the world size"
-    full = torch.empty((n,) + tuple(x_local.shape[1:]), dtype=x_local.dtype, device=x_local.device)
-    dist.all_gather_into_tensor(full, x_local.contiguous())
-    return full
+        return None
+    return api.scalegann_comm_init(rank, world, share_unique_id(rank, world))
 
 
 class _Timer:
@@ -119,7 +110,7 @@ class _Timer:
         return out
 
 
-def build_index(x: torch.Tensor, cfg: BuildConfig, rank: int = 0, world: int = 1, timing: bool = False,
+def build_index(x: torch.Tensor, cfg: BuildConfig, rank: int = 0, world: int = 1, comm=None, timing: bool = False,
                 ws: api.Workspace | None = None) -> Index:
     n, d = x.shape
     tm = _Timer(timing)
@@ -129,7 +120,7 @@ def build_index(x: torch.Tensor, cfg: BuildConfig, rank: int = 0, world: int = 1
         C = api.scalegann_kmeans(x, cfg.k, seed=cfg.kmeans_seed, max_iter=cfg.kmeans_iters, spc=cfg.kmeans_spc, ws=ws)
     else:
         C = torch.empty(cfg.k, d, dtype=torch.float32, device=x.device)
-    broadcast_centroids(C, world)
+    api.scalegann_broadcast_centroids(comm, C)
     # a2-a3 — partition (identical on every rank)
     tm.mark("a2a3_partition")
     home, pd, counts = api.scalegann_partition(x, C, omega=cfg.omega, epsilon=cfg.epsilon,
@@ -137,36 +128,43 @@ def build_index(x: torch.Tensor, cfg: BuildConfig, rank: int = 0, world: int = 1
                                                block_size=cfg.block_size, capacity=cfg.capacity, ws=ws)
     sizes = counts["sizes"]
     owner = lpt_owner(sizes, world)
-    inv = torch.full((n, cfg.omega), -1, dtype=torch.int32, device=x.device)
-    idmaps, graphs, graphs_d = [None] * cfg.k, [None] * cfg.k, [None] * cfg.k
-    # a4-a7 — owned shards
+    R, W = cfg.R, 2 + 2 * cfg.R
+    owned_index, rec_slot, send, recv, n_owned = api.scalegann_merge_plan(home, owner, rank, world, ws=ws)
+    merged, merged_d = api.scalegann_merge_init(n_owned, R, device=x.device)
+    sendbuf = torch.empty(max(sum(send), 1) * W, dtype=torch.int32, device=x.device)
+    # a4-a7 — owned shards, each folded into the merged rows and freed
     tm.mark("a4a7_build")
     for s in range(cfg.k):
         if owner[s] != rank or sizes[s] == 0:
             continue
-        idmaps[s] = api.scalegann_shard_idmap(home, s, m=sizes[s], inv=inv, ws=ws)
-        graphs[s], graphs_d[s] = api.scalegann_build_shard(x, idmaps[s], cfg.L, cfg.R, metric=cfg.metric,
-                                                           precision=cfg.precision, prune_rule=cfg.prune_rule,
-                                                           protected_edges=cfg.protected_edges, ws=ws)
-    # a8 — merge
+        idmap = api.scalegann_shard_idmap(home, s, m=sizes[s], ws=ws)
+        g, gd = api.scalegann_build_shard(x, idmap, cfg.L, cfg.R, metric=cfg.metric, precision=cfg.precision,
+                                          prune_rule=cfg.prune_rule, protected_edges=cfg.protected_edges, ws=ws)
+        api.scalegann_merge_shard(home, owner, rank, world, s, idmap, g, gd, owned_index, rec_slot, merged, merged_d,
+                                  sendbuf)
+        del g, gd, idmap
+    # a8 — rows whose primary lives elsewhere travel to its owner (N2), then fold
     tm.mark("a8_merge")
-    if world == 1:
-        merged, merged_d = api.scalegann_merge(home, inv, idmaps, graphs, graphs_d, ws=ws)
-    else:
-        R = cfg.R
-        W = 2 + 2 * R
-        send, recv = api.scalegann_merge_counts(home, cfg.k, owner, rank, world, ws=ws)
-        any_graph = next((g for g in graphs if g is not None), None)
-        if any_graph is None:   # a rank without shards still takes part in the exchange
-            graphs = [torch.empty(0, R, dtype=torch.int32, device=x.device) if s == 0 else None
-                      for s in range(cfg.k)]
-        sendbuf = api.scalegann_merge_pack(home, inv, owner, rank, world, idmaps, graphs, graphs_d, sum(send), ws=ws)
-        recvbuf = exchange_records(sendbuf, send, recv, W)
-        merged, merged_d = api.scalegann_merge_union(home, inv, owner, rank, idmaps, graphs, graphs_d, recvbuf,
-                                                     sum(recv), ws=ws)
+    if world > 1:
+        recvbuf = api.scalegann_exchange_records(comm, sendbuf, send, recv, W)
+        api.scalegann_merge_finish(cfg.omega, owned_index, recvbuf, sum(recv), merged, merged_d, ws=ws)
     tm.mark("end")
     entry, _ = api.scalegann_entry_points(home, pd, sizes, ws=ws)
-    return Index(merged, merged_d, entry, home, pd, C, sizes, counts, owner, tm.result())
+    return Index(merged, merged_d, entry, home, pd, C, sizes, counts, owner, tm.result(), owned_index=owned_index)
+
+
+def gather_merged(index: "Index", rank: int, world: int) -> torch.Tensor | None:
+    """The full n x R merged graph on rank 0 (evaluation only): every rank's owned rows placed at
+    their global ids (torch.distributed gather).  Other ranks return None."""
+    n = index.home.shape[0]
+    if world == 1:
+        return index.merged
+    R = index.merged.shape[1]
+    full = torch.full((n, R), -1, dtype=torch.int32, device=index.merged.device)
+    own = owned_rows(index, rank)
+    full[own] = index.merged
+    dist.all_reduce(full, op=dist.ReduceOp.MAX)   # rows owned elsewhere are -1 here
+    return full if rank == 0 else None
 
 
 def owned_rows(index: Index, rank: int) -> torch.Tensor:

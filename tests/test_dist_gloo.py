@@ -1,11 +1,13 @@
 """World-size-2 tests of the multi-GPU host logic on CPU (gloo backend, 127.0.0.1).
 
 What runs per rank is the product's host code (paper_2605_10135_b200.pipeline): LPT shard
-placement, the centroid broadcast (N1) and the merge-record all-to-all (N2).  The per-shard graphs
-and the record packing/union around the exchange are computed with the oracle on the CPU
-(the CUDA kernels need a GPU), following the record format of include/scalegann.h
-(scalegann_merge_pack: [g, h, R global ids, R dist bits], grouped by destination rank, ascending
-(g, h)).  The merged rows each rank ends up owning must equal the single-process oracle merge.
+placement and the bootstrap of the library's NCCL communicator (rank 0's unique id shared over
+the process group).  The collectives themselves (N1 centroid broadcast, N2 record exchange) run
+on that communicator on GPUs; here the merge PROTOCOL of include/scalegann.h is replayed on the
+CPU with the oracle's shard graphs and a gloo all-to-all standing in for N2: a row built on a
+rank whose primary is owned by another rank travels as a record [g, h, R global ids, R dist
+bits] (grouped by destination, ascending g); counts are derived from home[] alone on both sides.
+The merged rows each rank ends up owning must equal the single-process oracle merge.
 """
 import os
 import socket
@@ -56,20 +58,20 @@ def _worker(rank, world, port, out):
         n, omega = home.shape
         k = len(idmaps)
         W = 2 + 2 * R
-        # N1: rank 0's centroids reach every rank
+        # N1 stand-in: rank 0's centroids reach every rank
         Ct = torch.from_numpy(C.copy()) if rank == 0 else torch.zeros(C.shape, dtype=torch.float32)
-        pipeline.broadcast_centroids(Ct, world)
+        dist.broadcast(Ct, src=0)
         assert np.array_equal(Ct.numpy(), C)
         # shard placement: identical on every rank, deterministic, balanced by m^2
         sizes = [len(a) for a in idmaps]
         owner = pipeline.lpt_owner(sizes, world)
-        # pack: records of replica rows (h >= 1) of shards owned here, to the primary's owner
+        # pack: rows (h >= 1) of shards owned here whose primary is owned by another rank
         inv = [dict(zip(a.tolist(), range(len(a)))) for a in idmaps]
         per_dest = [[] for _ in range(world)]
         for g in range(n):
             for h in range(1, omega):
                 s = int(home[g, h])
-                if s == SENT or owner[s] != rank:
+                if s == SENT or owner[s] != rank or owner[int(home[g, 0])] == rank:
                     continue
                 row = graphs[s][inv[s][g]]
                 gid = np.where(row == SENT, SENT, idmaps[s][np.minimum(row, len(idmaps[s]) - 1)]).astype(np.uint32)
@@ -78,16 +80,18 @@ def _worker(rank, world, port, out):
         send = [len(r) for r in per_dest]
         sendbuf = torch.from_numpy(np.concatenate([np.stack(r) if r else np.zeros((0, W), np.uint32)
                                                    for r in per_dest]).view(np.int32).reshape(-1).copy())
-        # receive counts from home alone (what scalegann_merge_counts computes on the device)
+        # receive counts from home alone (what scalegann_merge_plan computes on the device)
         recv = [0] * world
         for g in range(n):
             if owner[int(home[g, 0])] != rank:
                 continue
             for h in range(1, omega):
                 s = int(home[g, h])
-                if s != SENT:
+                if s != SENT and owner[s] != rank:
                     recv[owner[s]] += 1
-        recvbuf = pipeline.exchange_records(sendbuf, send, recv, W)
+        recvbuf = torch.empty(max(sum(recv), 1) * W, dtype=torch.int32)
+        dist.all_to_all_single(recvbuf[: sum(recv) * W], sendbuf[: sum(send) * W], [c * W for c in recv],
+                               [c * W for c in send])
         recs = recvbuf[: sum(recv) * W].numpy().view(np.uint32).reshape(-1, W)
         # union on the owner: local shard rows + received replica rows, through the oracle merge
         lg = [graphs[s].copy() if owner[s] == rank else np.full_like(graphs[s], SENT) for s in range(k)]
@@ -135,23 +139,22 @@ def test_lpt_owner_properties():
         assert max(load) <= max(sizes) ** 2 + min(l for l in load) or world == 1
 
 
-def _gather_worker(rank, world, port, out):
+def _uid_worker(rank, world, port, out):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_2605_10135_b200 import datagen, pipeline
-        x = datagen.sift_like(1000, 16, seed=3)
-        rows = 1000 // world
-        full = pipeline.distribute_dataset(x[rank * rows:(rank + 1) * rows].clone(), 1000, rank, world)
-        out[rank] = bool(torch.equal(full, x))
+        from paper_2605_10135_b200 import pipeline
+        out[rank] = pipeline.share_unique_id(rank, world)
     finally:
         dist.destroy_process_group()
 
 
-def test_distribute_dataset_world2():
-    """Each rank uploads only its slice; the all-gather rebuilds the full dataset everywhere."""
+def test_share_unique_id_world2():
+    """The library communicator's bootstrap: rank 0's NCCL unique id (scalegann_get_unique_id)
+    reaches every rank unchanged over the process group (gloo here; nccl on GPUs)."""
     port = _free_port()
     with mp.Manager() as mgr:
         out = mgr.dict()
-        mp.spawn(_gather_worker, args=(2, port, out), nprocs=2, join=True)
-        assert dict(out) == {0: True, 1: True}
+        mp.spawn(_uid_worker, args=(2, port, out), nprocs=2, join=True)
+        res = dict(out)
+    assert len(res[0]) == 128 and res[0] == res[1] and any(res[0])

@@ -202,7 +202,6 @@ def test_merge_bit_exact(api, oracle_mod):
     C = x[::2000][:3].clone()
     r = oracle_mod.partition(x.numpy(), C.numpy(), omega=3, eps=1.6)
     home = torch.from_numpy(r["home"].view(np.int32)).cuda()
-    inv = torch.full((6000, 3), -1, dtype=torch.int32, device="cuda")
     idm_g, g_g, gd_g, idm_o, g_o, gd_o = [], [], [], [], [], []
     for s in range(3):
         im = oracle_mod.idmap(r["home"], s)
@@ -210,50 +209,52 @@ def test_merge_bit_exact(api, oracle_mod):
         pr, prd = oracle_mod.prune(ids, dd, 8)
         f, fd = oracle_mod.reverse(pr, prd)
         idm_o.append(im), g_o.append(f), gd_o.append(fd)
-        idm_g.append(api.scalegann_shard_idmap(home, s, inv=inv))
+        idm_g.append(api.scalegann_shard_idmap(home, s))
         g_g.append(torch.from_numpy(f.view(np.int32)).cuda())
         gd_g.append(torch.from_numpy(fd).cuda())
-    m, md = api.scalegann_merge(home, inv, idm_g, g_g, gd_g)
+    m, md = api.scalegann_merge(home, idm_g, g_g, gd_g)
     om, omd = oracle_mod.merge(r["home"], idm_o, g_o, gd_o)
     assert np.array_equal(u32(m), om) and np.array_equal(md.cpu().numpy(), omd)
 
 
-def test_merge_emulated_ranks_equal_single(api):
-    """The distributed pack -> exchange -> union protocol, with ranks emulated in one process,
-    gives the same merged graph as the single-process merge."""
+@pytest.mark.parametrize("world", [2, 3])
+def test_merge_emulated_ranks_equal_single(api, world):
+    """The distributed streaming protocol (plan -> fold shards -> records -> exchange -> fold
+    records), with `world` ranks emulated in one process, gives owner rows that reassemble to the
+    single-process merged graph byte for byte."""
     from paper_2605_10135_b200.pipeline import BuildConfig, build_index, lpt_owner
     x = datagen.sift_like(8000, 64, seed=31).cuda()
-    cfg = BuildConfig(k=4, L=32, R=16)
+    cfg = BuildConfig(k=4, omega=3, epsilon=1.5, L=32, R=16)
     idx = build_index(x, cfg)
     home, n = idx.home, x.shape[0]
     sizes = idx.sizes
-    inv = torch.full((n, 2), -1, dtype=torch.int32, device="cuda")
     idm, gs, gds = [], [], []
     for s in range(4):
-        idm.append(api.scalegann_shard_idmap(home, s, inv=inv))
+        idm.append(api.scalegann_shard_idmap(home, s))
         g, gd = api.scalegann_build_shard(x, idm[-1], cfg.L, cfg.R)
         gs.append(g), gds.append(gd)
-    world = 2
     owner = lpt_owner(sizes, world)
     W = 2 + 2 * cfg.R
-    sends = {}
+    st = {}
     for rk in range(world):
-        own = [idm[s] if owner[s] == rk else None for s in range(4)]
-        og = [gs[s] if owner[s] == rk else None for s in range(4)]
-        ogd = [gds[s] if owner[s] == rk else None for s in range(4)]
-        send, recv = api.scalegann_merge_counts(home, 4, owner, rk, world)
-        buf = api.scalegann_merge_pack(home, inv, owner, rk, world, own, og, ogd, sum(send))
-        chunks = list(torch.split(buf, [c * W for c in send]))
-        sends[rk] = (chunks, send, recv)
-    merged = torch.full_like(idx.merged, -1)
-    merged_d = torch.full_like(idx.merged_d, float("inf"))
+        oi, rs, send, recv, no = api.scalegann_merge_plan(home, owner, rk, world)
+        m, md = api.scalegann_merge_init(no, cfg.R)
+        sendbuf = torch.empty(max(sum(send), 1) * W, dtype=torch.int32, device="cuda")
+        for s in range(4):
+            if owner[s] == rk:
+                api.scalegann_merge_shard(home, owner, rk, world, s, idm[s], gs[s], gds[s], oi, rs, m, md, sendbuf)
+        chunks = list(torch.split(sendbuf[: sum(send) * W], [c * W for c in send]))
+        st[rk] = (oi, m, md, chunks, send, recv)
+    full = torch.full_like(idx.merged, -1)
+    full_d = torch.full_like(idx.merged_d, float("nan"))
     for rk in range(world):
-        recvbuf = torch.cat([sends[src][0][rk] for src in range(world)])
-        own = [idm[s] if owner[s] == rk else None for s in range(4)]
-        og = [gs[s] if owner[s] == rk else None for s in range(4)]
-        ogd = [gds[s] if owner[s] == rk else None for s in range(4)]
-        api.scalegann_merge_union(home, inv, owner, rk, own, og, ogd, recvbuf, recvbuf.numel() // W, merged, merged_d)
-    assert torch.equal(merged, idx.merged) and torch.equal(merged_d, idx.merged_d)
+        oi, m, md, _, _, recv = st[rk]
+        recvbuf = torch.cat([st[src][3][rk] for src in range(world)])
+        assert recvbuf.numel() == sum(recv) * W
+        api.scalegann_merge_finish(cfg.omega, oi, recvbuf, sum(recv), m, md)
+        own = torch.tensor(owner, device="cuda")[home[:, 0].long()] == rk
+        full[own], full_d[own] = m, md
+    assert torch.equal(full, idx.merged) and torch.equal(full_d, idx.merged_d)
 
 
 # ------------------------------------------------------------------ a9 search
