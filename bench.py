@@ -43,8 +43,10 @@ def parse():
                     help="C1: BASELINE configs[1] weak-scaled (1M x 128 and 4 shards per GPU, the driver's line); "
                          "C2/C3/C4: the fixed 8-shard workloads of SURVEY 8(d) on any number of GPUs")
     ap.add_argument("--n-per-gpu", type=int, default=1_000_000)
+    ap.add_argument("--n", type=int, default=0, help="C2-C4: override the dataset size (reduced runs)")
     ap.add_argument("--shards-per-gpu", type=int, default=4)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e", action="store_true", help="C2-C4: also time the host-buffer e2e leg")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-recall", action="store_true")
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle parity check at bench size")
@@ -299,10 +301,11 @@ def main():
         args.no_e2e = args.no_cpu_baseline = args.no_recall = True
 
     kind, n_fix, d, k_fix, scaling = CONFIGS[args.config]
-    n = n_fix if n_fix else args.n_per_gpu * world
+    n = (args.n or n_fix) if n_fix else args.n_per_gpu * world
     k = k_fix if k_fix else args.shards_per_gpu * world
-    if args.config != "C1":   # big workloads: evaluation legs off unless asked
+    if args.config != "C1":   # big workloads: the oracle leg and the pinned-host e2e copy off unless asked
         args.no_cpu_baseline = True
+        args.no_e2e = args.no_e2e or not args.e2e
     cfg = BuildConfig(k=k, omega=2, L=128, R=64)
     x = datagen._make(kind, n, d, datagen.DATA_SEED, "cuda")
     torch.cuda.synchronize()
@@ -413,7 +416,8 @@ def main():
     if not args.no_recall:
         full = gather_merged(idx, rank, world)
         if rank == 0:
-            q = datagen._make(kind, 10_000, d, datagen.DATA_SEED + datagen.QUERY_SEED_OFFSET, "cuda")
+            nq = 10_000 if args.config == "C1" else 1000
+            q = datagen._make(kind, nq, d, datagen.DATA_SEED + datagen.QUERY_SEED_OFFSET, "cuda")
             recall = {}
             gt = None
             for beam in (32, 64, 128):

@@ -103,10 +103,12 @@ static size_t knn_total_ws(uint64_t ma, uint64_t mb, uint32_t d, int prec, uint3
     return b + knn_core_workspace(L, ma, d, prec, SG_L2) + 2 * (ma * 4 + 256) + (same ? order_workspace(ma, d, prec, SG_L2) : 0) + 4096;
 }
 
-static int worst_prec(sg_dtype dtype, int32_t precision) {
-    // AUTO resolves at run time; size the workspace for the widest candidate
+static int worst_prec(sg_dtype dtype, int32_t precision, uint32_t d) {
+    // AUTO resolves at run time; size the workspace for the widest candidate.  u8 data is
+    // F16_EXACT whenever 2 d 255^2 < 2^24 (gather.cu resolves it without looking at the data)
     if (precision != SG_PREC_AUTO) return precision;
-    return dtype == SG_U8 ? SG_PREC_TF32 : SG_PREC_TF32;
+    if (dtype == SG_U8 && 2ull * d * 255 * 255 < (1ull << 24)) return SG_PREC_F16_EXACT;
+    return SG_PREC_TF32;
 }
 
 static sg_status check_knn_shape(int prec, int metric, uint32_t d, uint32_t L) {
@@ -216,7 +218,7 @@ sg_status scalegann_entry_points(const uint32_t* home, const float* primary_d, u
 sg_status scalegann_knn_workspace(uint64_t ma, uint64_t mb, uint32_t d, sg_dtype dtype, uint32_t L, int32_t precision,
                                   size_t* bytes) {
     SG_CHECK_ARG(bytes, "null bytes");
-    const int pr = worst_prec(dtype, precision);
+    const int pr = worst_prec(dtype, precision, d);
     *bytes = knn_total_ws(ma, mb, d, pr, L, false) + (ma == mb ? order_workspace(ma, d, pr, SG_L2) : 0);
     return SG_OK;
 }
@@ -294,7 +296,7 @@ sg_status scalegann_reverse(const uint32_t* pruned, const float* pruned_d, uint6
 
 // ------------------------------------------------------------------ a4-a7
 static size_t build_ws(uint64_t m, uint32_t d, sg_dtype dtype, const sg_build_params* p) {
-    const int prec = worst_prec(dtype, p->precision);
+    const int prec = worst_prec(dtype, p->precision, d);
     size_t b = 1024;
     b += 2 * (m * p->L * 4 + 256);     // kNN ids + dists (when not caller-provided)
     b += 2 * (m * p->R * 4 + 256);     // pruned ids + dists
@@ -502,7 +504,7 @@ sg_status scalegann_search_workspace(uint64_t n, uint32_t d, sg_dtype dtype, uin
                                      size_t* bytes) {
     SG_CHECK_ARG(bytes, "null bytes");
     (void)beam;
-    size_t gt = knn_total_ws(nq, n, d, worst_prec(dtype, SG_PREC_AUTO), topk, false) + (size_t)nq * topk * 8 + 512;
+    size_t gt = knn_total_ws(nq, n, d, worst_prec(dtype, SG_PREC_AUTO, d), topk, false) + (size_t)nq * topk * 8 + 512;
     size_t bs = beam_ws(n, nq) + (size_t)nq * topk * 4 + 1024;
     *bytes = gt + bs;
     return SG_OK;

@@ -63,7 +63,8 @@ uint32_t order_groups(uint64_t m) {
 }
 
 size_t order_workspace(uint64_t m, uint32_t d, int prec, int metric) {
-    const uint32_t kc = order_groups(m) ? order_groups(m) : 1;
+    if (order_groups(m) < 2) return 0;   // ordering off (the default): no scratch
+    const uint32_t kc = order_groups(m);
     Carver cv(nullptr, 0);
     cv.take<uint32_t>(kc);          // centroid row ids
     cv.take<uint32_t>(m);           // assignment
