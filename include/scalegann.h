@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define SCALEGANN_ABI_VERSION 1
+#define SCALEGANN_ABI_VERSION 2
 #define SG_SENTINEL 0xFFFFFFFFu
 
 typedef enum {
@@ -250,17 +250,23 @@ sg_status scalegann_merge(void* comm, const uint32_t* home, uint64_t n, uint32_t
 
 /* ---- a9: recall evaluation (reading R14) ------------------
  * Greedy best-first beam search from `entry` over graph (n x R global ids) for
- * nq queries (nq x d, same dtype as x); out_ids nq x topk.  gt (nq x topk,
- * device) may be NULL, then it is computed exactly with scalegann_knn and
- * written to gt_out (if not NULL).  recall_host = |ret & gt| / (nq*topk);
- * synchronises.  beam <= 512, topk <= beam, R <= 128. */
+ * nq queries (nq x d, same dtype as x); out_ids nq x topk.  Distances are P8's
+ * exact ones (u8: integer; f32: fp64 sum of the squared differences, one
+ * rounding to f32), so result lists equal the oracle's.  gt (nq x topk, device)
+ * may be NULL, then it is computed exactly with scalegann_knn and written to
+ * gt_out (if not NULL).  recall_host = |ret & gt| / (nq*topk); n_dist_host
+ * (may be NULL) = distance computations over all queries (P:515-516's proxy of
+ * search work); both synchronise.  beam <= 512, topk <= beam, R <= 128.  The
+ * visited set is a bitmap of n bits per query, or a hash set of 8 x beam x R
+ * ids when that is smaller; a hash set that fills up returns SG_ERR_WORKSPACE. */
 sg_status scalegann_search_workspace(uint64_t n, uint32_t d, sg_dtype dtype, uint32_t nq, uint32_t topk,
                                      uint32_t beam, size_t* bytes);
 sg_status scalegann_search_eval(const void* x, sg_dtype dtype, uint64_t n, uint32_t d,
                                 const uint32_t* graph, uint32_t R, uint32_t entry, const void* queries,
                                 uint32_t nq, uint32_t topk, uint32_t beam, int32_t metric,
                                 const uint32_t* gt, uint32_t* gt_out, uint32_t* out_ids,
-                                double* recall_host, void* ws, size_t ws_bytes, void* stream);
+                                double* recall_host, uint64_t* n_dist_host, void* ws, size_t ws_bytes,
+                                void* stream);
 
 /* ---- a9, split-only mode: per-shard search + result merge (§8(f) NEXT-2;
  * reading R15) ------------------------------------------------------------------
@@ -268,17 +274,17 @@ sg_status scalegann_search_eval(const void* x, sg_dtype dtype, uint64_t n, uint3
  * points (entries_host, host, e.g. every shard's entry from scalegann_entry_points), each
  * keeping its own beam; the per-entry top-topk lists are merged into the topk smallest
  * distinct (dist, id).  For a split-only graph (omega = 1, disjoint shards) this is "search
- * every shard and merge the results".  Errors as scalegann_search_eval, plus
- * SG_ERR_INVALID_ARG for n_entries outside [1, 1024] or an entry >= n.  Synchronises when
- * recall_host is not NULL. */
+ * every shard and merge the results".  SENTINEL entries (empty shards) are skipped.  Errors as
+ * scalegann_search_eval, plus SG_ERR_INVALID_ARG for n_entries outside [1, 1024], an entry >= n
+ * that is not SENTINEL, or no real entry.  Synchronises when recall_host or n_dist_host is set. */
 sg_status scalegann_search_shards_workspace(uint64_t n, uint32_t d, sg_dtype dtype, uint32_t nq, uint32_t topk,
                                             uint32_t beam, uint32_t n_entries, size_t* bytes);
 sg_status scalegann_search_eval_shards(const void* x, sg_dtype dtype, uint64_t n, uint32_t d,
                                        const uint32_t* graph, uint32_t R, const uint32_t* entries_host,
                                        uint32_t n_entries, const void* queries, uint32_t nq, uint32_t topk,
                                        uint32_t beam, int32_t metric, const uint32_t* gt, uint32_t* gt_out,
-                                       uint32_t* out_ids, double* recall_host, void* ws, size_t ws_bytes,
-                                       void* stream);
+                                       uint32_t* out_ids, double* recall_host, uint64_t* n_dist_host,
+                                       void* ws, size_t ws_bytes, void* stream);
 
 /* ---- diagnostics ------------------------------------------------------------
  * Raw distance-tile probe of the tcgen05 GEMM core (validation of the MMA

@@ -109,10 +109,10 @@ def load(build_if_missing: bool = True):
                              vp], i32),
         "scalegann_search_workspace": ([u64, u32, i32, u32, u32, u32, psz], i32),
         "scalegann_search_eval": ([vp, i32, u64, u32, vp, u32, u32, vp, u32, u32, u32, i32, vp, vp, vp,
-                                   P(ctypes.c_double), vp, sz, vp], i32),
+                                   P(ctypes.c_double), pu64, vp, sz, vp], i32),
         "scalegann_search_shards_workspace": ([u64, u32, i32, u32, u32, u32, u32, psz], i32),
         "scalegann_search_eval_shards": ([vp, i32, u64, u32, vp, u32, P(u32), u32, vp, u32, u32, u32, i32, vp, vp,
-                                          vp, P(ctypes.c_double), vp, sz, vp], i32),
+                                          vp, P(ctypes.c_double), pu64, vp, sz, vp], i32),
         "scalegann_gemm_probe": ([vp, u64, vp, u64, i32, u32, i32, vp, vp, sz, vp], i32),
         "scalegann_stats_enable": ([ctypes.c_int], i32),
         "scalegann_knn_profile": ([vp], i32),
@@ -478,9 +478,20 @@ def scalegann_knn_profile(counters=None):
 
 
 # ----------------------------------------------------------------------------- a9
-def scalegann_search_eval(x, graph, entry, queries, topk=10, beam=64, metric=SG_L2, gt=None, ws=None):
-    """Returns (out_ids nq x topk, gt nq x topk, recall)."""
+def _search_checks(x, graph, queries):
+    _dev(x, "x")
+    _dev(graph, "graph")
+    _dev(queries, "queries")
+    if queries.dtype != x.dtype or queries.shape[1] != x.shape[1]:
+        raise ValueError(f"queries must match x in dtype and width ({queries.dtype} {tuple(queries.shape)} vs "
+                         f"{x.dtype} {tuple(x.shape)})")
+
+
+def scalegann_search_eval(x, graph, entry, queries, topk=10, beam=64, metric=SG_L2, gt=None, ws=None,
+                          return_ndist=False):
+    """Returns (out_ids nq x topk, gt nq x topk, recall[, distance computations])."""
     L = load()
+    _search_checks(x, graph, queries)
     n, d = x.shape
     R = graph.shape[1]
     nq = queries.shape[0]
@@ -489,18 +500,22 @@ def scalegann_search_eval(x, graph, entry, queries, topk=10, beam=64, metric=SG_
     if gt is None:
         gt_out = torch.empty(nq, topk, dtype=torch.int32, device=x.device)
     rec = ctypes.c_double(0.0)
+    nd = ctypes.c_uint64(0)
     nb = _size_q(L.scalegann_search_workspace, n, d, _dtype(x), nq, topk, beam)
     p, nbytes = _ws(nb, ws)
     _check(L.scalegann_search_eval(_ptr(x), _dtype(x), n, d, _ptr(graph), R, entry, _ptr(queries), nq, topk, beam,
-                                   metric, _ptr(gt), _ptr(gt_out), _ptr(out), ctypes.byref(rec), p, nbytes,
-                                   _stream()))
-    return out, (gt if gt is not None else gt_out), rec.value
+                                   metric, _ptr(gt), _ptr(gt_out), _ptr(out), ctypes.byref(rec), ctypes.byref(nd), p,
+                                   nbytes, _stream()))
+    res = (out, (gt if gt is not None else gt_out), rec.value)
+    return res + (nd.value,) if return_ndist else res
 
 
-def scalegann_search_eval_shards(x, graph, entries, queries, topk=10, beam=64, metric=SG_L2, gt=None, ws=None):
+def scalegann_search_eval_shards(x, graph, entries, queries, topk=10, beam=64, metric=SG_L2, gt=None, ws=None,
+                                 return_ndist=False):
     """Split-only search: one beam per entry point, per-entry results merged.
-    Returns (out_ids nq x topk, gt nq x topk, recall)."""
+    Returns (out_ids nq x topk, gt nq x topk, recall[, distance computations])."""
     L = load()
+    _search_checks(x, graph, queries)
     n, d = x.shape
     R = graph.shape[1]
     nq = queries.shape[0]
@@ -511,9 +526,11 @@ def scalegann_search_eval_shards(x, graph, entries, queries, topk=10, beam=64, m
     if gt is None:
         gt_out = torch.empty(nq, topk, dtype=torch.int32, device=x.device)
     rec = ctypes.c_double(0.0)
+    nd = ctypes.c_uint64(0)
     nb = _size_q(L.scalegann_search_shards_workspace, n, d, _dtype(x), nq, topk, beam, ne)
     p, nbytes = _ws(nb, ws)
     _check(L.scalegann_search_eval_shards(_ptr(x), _dtype(x), n, d, _ptr(graph), R, ent, ne, _ptr(queries), nq, topk,
-                                          beam, metric, _ptr(gt), _ptr(gt_out), _ptr(out), ctypes.byref(rec), p,
-                                          nbytes, _stream()))
-    return out, (gt if gt is not None else gt_out), rec.value
+                                          beam, metric, _ptr(gt), _ptr(gt_out), _ptr(out), ctypes.byref(rec),
+                                          ctypes.byref(nd), p, nbytes, _stream()))
+    res = (out, (gt if gt is not None else gt_out), rec.value)
+    return res + (nd.value,) if return_ndist else res

@@ -38,7 +38,7 @@ sg_status merge_finish_run(uint32_t omega, uint32_t R, const uint32_t* owned_ind
 sg_status comm_rank_world(void* comm, int* rank, int* world);
 sg_status exchange_records_run(void* comm, const uint32_t* sendbuf, const uint64_t* send_host, uint32_t* recvbuf,
                                const uint64_t* recv_host, uint32_t words, cudaStream_t st);
-size_t beam_ws(uint64_t n, uint32_t nq);
+size_t beam_ws(uint64_t n, uint32_t nq, uint32_t beam, uint32_t R);
 sg_status beam_run(const void* x, sg_dtype dtype, uint64_t n, uint32_t d, const uint32_t* graph, uint32_t R,
                    uint32_t entry, const void* q, uint32_t nq, uint32_t topk, uint32_t beam, int metric,
                    uint32_t* out_ids, unsigned long long* ndist, Carver& cv, cudaStream_t st,
@@ -505,7 +505,7 @@ sg_status scalegann_search_workspace(uint64_t n, uint32_t d, sg_dtype dtype, uin
     SG_CHECK_ARG(bytes, "null bytes");
     (void)beam;
     size_t gt = knn_total_ws(nq, n, d, worst_prec(dtype, SG_PREC_AUTO, d), topk, false) + (size_t)nq * topk * 8 + 512;
-    size_t bs = beam_ws(n, nq) + (size_t)nq * topk * 4 + 1024;
+    size_t bs = beam_ws(n, nq, beam, 128) + (size_t)nq * topk * 4 + 1024;   // sized for R <= 128
     *bytes = gt + bs;
     return SG_OK;
 }
@@ -513,7 +513,7 @@ sg_status scalegann_search_workspace(uint64_t n, uint32_t d, sg_dtype dtype, uin
 sg_status scalegann_search_eval(const void* x, sg_dtype dtype, uint64_t n, uint32_t d, const uint32_t* graph, uint32_t R,
                                 uint32_t entry, const void* queries, uint32_t nq, uint32_t topk, uint32_t beam,
                                 int32_t metric, const uint32_t* gt, uint32_t* gt_out, uint32_t* out_ids,
-                                double* recall_host, void* ws, size_t ws_bytes, void* stream) {
+                                double* recall_host, uint64_t* n_dist_host, void* ws, size_t ws_bytes, void* stream) {
     SG_CHECK_ARG(x && graph && queries && out_ids && nq > 0 && n > 0 && d > 0 && d <= 1024, "search: bad arguments");
     SG_CHECK_ARG(entry < n, "search: entry out of range");
     SG_CHECK_ARG(R >= 1 && R <= 128 && topk >= 1 && topk <= beam && beam <= 512, "search: need R<=128, topk<=beam<=512");
@@ -530,7 +530,14 @@ sg_status scalegann_search_eval(const void* x, sg_dtype dtype, uint64_t n, uint3
                         kc.base ? kc.base + kc.off : nullptr, kc.cap > kc.off ? kc.cap - kc.off : 0, st));
         g = gbuf;
     }
-    SG_TRY(beam_run(x, dtype, n, d, graph, R, entry, queries, nq, topk, beam, metric, out_ids, nullptr, cv, st));
+    unsigned long long* nd = cv.take<unsigned long long>(1);
+    if (!cv.ok()) { set_error("search: workspace too small"); return SG_ERR_WORKSPACE; }
+    SG_CUDA(cudaMemsetAsync(nd, 0, sizeof(unsigned long long), st));
+    SG_TRY(beam_run(x, dtype, n, d, graph, R, entry, queries, nq, topk, beam, metric, out_ids, nd, cv, st));
+    if (n_dist_host) {
+        SG_CUDA(cudaMemcpyAsync(n_dist_host, nd, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+        SG_CUDA(cudaStreamSynchronize(st));
+    }
     if (recall_host) return recall_run(out_ids, g, nq, topk, recall_host, cv, st);
     return SG_OK;
 }
@@ -546,11 +553,18 @@ sg_status scalegann_search_eval_shards(const void* x, sg_dtype dtype, uint64_t n
                                        uint32_t R, const uint32_t* entries_host, uint32_t n_entries,
                                        const void* queries, uint32_t nq, uint32_t topk, uint32_t beam,
                                        int32_t metric, const uint32_t* gt, uint32_t* gt_out, uint32_t* out_ids,
-                                       double* recall_host, void* ws, size_t ws_bytes, void* stream) {
+                                       double* recall_host, uint64_t* n_dist_host, void* ws, size_t ws_bytes,
+                                       void* stream) {
     SG_CHECK_ARG(x && graph && queries && out_ids && entries_host && nq > 0 && n > 0 && d > 0 && d <= 1024,
                  "search_shards: bad arguments");
     SG_CHECK_ARG(n_entries >= 1 && n_entries <= 1024, "search_shards: need 1 <= n_entries <= 1024");
-    for (uint32_t s = 0; s < n_entries; s++) SG_CHECK_ARG(entries_host[s] < n, "search_shards: entry out of range");
+    // SENTINEL entries (empty shards, scalegann_entry_points) are skipped; at least one is needed
+    uint32_t n_real = 0;
+    for (uint32_t s = 0; s < n_entries; s++) {
+        SG_CHECK_ARG(entries_host[s] < n || entries_host[s] == SG_SENT, "search_shards: entry out of range");
+        n_real += entries_host[s] != SG_SENT;
+    }
+    SG_CHECK_ARG(n_real >= 1, "search_shards: every entry is SENTINEL");
     SG_CHECK_ARG(R >= 1 && R <= 128 && topk >= 1 && topk <= beam && beam <= 512, "search: need R<=128, topk<=beam<=512");
     SG_CHECK_ARG(metric == SG_L2 || metric == SG_IP, "search: bad metric");
     cudaStream_t st = S(stream);
@@ -567,12 +581,22 @@ sg_status scalegann_search_eval_shards(const void* x, sg_dtype dtype, uint64_t n
                         kc.base ? kc.base + kc.off : nullptr, kc.cap > kc.off ? kc.cap - kc.off : 0, st));
         g = gbuf;
     }
+    unsigned long long* nd = cv.take<unsigned long long>(1);
+    if (!cv.ok()) { set_error("search_shards: workspace too small"); return SG_ERR_WORKSPACE; }
+    SG_CUDA(cudaMemsetAsync(nd, 0, sizeof(unsigned long long), st));
+    uint32_t ns = 0;
     for (uint32_t s = 0; s < n_entries; s++) {
-        Carver bc = cv;   // every per-entry search reuses the same visited-bitmap scratch
-        SG_TRY(beam_run(x, dtype, n, d, graph, R, entries_host[s], queries, nq, topk, beam, metric, nullptr, nullptr,
-                        bc, st, keys + (size_t)s * nq * topk));
+        if (entries_host[s] == SG_SENT) continue;
+        Carver bc = cv;   // every per-entry search reuses the same visited-set scratch
+        SG_TRY(beam_run(x, dtype, n, d, graph, R, entries_host[s], queries, nq, topk, beam, metric, nullptr, nd, bc, st,
+                        keys + (size_t)ns * nq * topk));
+        ns++;
     }
-    SG_TRY(shard_merge_run(keys, n_entries, nq, topk, out_ids, st));
+    SG_TRY(shard_merge_run(keys, ns, nq, topk, out_ids, st));
+    if (n_dist_host) {
+        SG_CUDA(cudaMemcpyAsync(n_dist_host, nd, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+        SG_CUDA(cudaStreamSynchronize(st));
+    }
     if (recall_host) return recall_run(out_ids, g, nq, topk, recall_host, cv, st);
     return SG_OK;
 }

@@ -4,10 +4,13 @@
 //
 // One warp per query.  The pool (<= beam entries, keys (ord(dist) << 32 | id)) stays sorted in
 // shared memory; each expansion takes the lowest unexpanded entry, marks its unvisited
-// neighbours in a per-query visited bitmap (global memory, one bit per vector), computes their
-// distances (lane per neighbour), sorts the new keys and merges them into the pool by rank
-// (binary search in both lists), truncating to beam — the same semantics as sorting the union
-// by (dist, id) and truncating.
+// neighbours in the query's visited set, computes their distances (lane per neighbour), sorts
+// the new keys and merges them into the pool by rank (binary search in both lists), truncating
+// to beam — the same semantics as sorting the union by (dist, id) and truncating.
+// Distances follow P4/P8 exactly: u8 rows in integer arithmetic, f32 rows as the sequential fp64
+// sum of the squared differences (products), rounded once to f32 — the oracle's definition.
+// The visited set is a bitmap over the n vectors (small n) or an open-addressing hash set of
+// ids (large n; 8 x beam x R slots per query, overflow reported), whichever is smaller.
 #include "common.cuh"
 
 namespace sg {
@@ -19,58 +22,83 @@ struct SearchArgs {
     const void* x;
     const void* q;
     const uint32_t* graph;
-    uint32_t* visited;     // batch x words
+    uint32_t* visited;     // batch x words: bitmap (hash == 0) or hash slots (hash == 1)
     uint32_t* out_ids;     // may be NULL when out_keys is set
     uint64_t* out_keys;    // optional: the first topk pool keys (ord(dist) << 32 | id), ~0 past np
     uint64_t n, words;
     uint32_t d, R, entry, nq, q0, topk, beam, poolcap, newcap;
     int dtype, metric;
+    int hash;              // visited set: 0 bitmap of n bits, 1 hash set of `words` slots
     unsigned long long* ndist;
+    int* overflow;         // set when a hash set fills up
 };
 
+// P4 / P8 exact distance of query qv (kept as loaded: u8 codes or f32) to row v
 __device__ __forceinline__ float qdist(const SearchArgs& a, const float* qv, uint32_t v) {
-    float s = 0.f;
-    if (a.dtype == SG_U8 && (a.d & 15) == 0 && ((uintptr_t)a.x & 15) == 0) {
-        // 16-byte loads of 16 codes, same sequential fmaf order as the scalar loop
-        const uint4* row = (const uint4*)((const uint8_t*)a.x + (uint64_t)v * a.d);
-        for (uint32_t j16 = 0; j16 < (a.d >> 4); j16++) {
-            const uint4 w = __ldg(row + j16);
-            const uint32_t wd[4] = {w.x, w.y, w.z, w.w};
-            const float* qq = qv + 16 * j16;
+    if (a.dtype == SG_U8) {
+        // integer arithmetic (exact: d * 255^2 < 2^31), rounded once to f32 like the oracle's int64
+        int s = 0;
+        if ((a.d & 15) == 0 && ((uintptr_t)a.x & 15) == 0) {
+            const uint4* row = (const uint4*)((const uint8_t*)a.x + (uint64_t)v * a.d);
+            for (uint32_t j16 = 0; j16 < (a.d >> 4); j16++) {
+                const uint4 w = __ldg(row + j16);
+                const uint32_t wd[4] = {w.x, w.y, w.z, w.w};
+                const float* qq = qv + 16 * j16;
 #pragma unroll
-            for (int b = 0; b < 16; b++) {
-                const float t = (float)((wd[b >> 2] >> (8 * (b & 3))) & 0xffu);
-                s = a.metric == SG_IP ? __fmaf_rn(-t, qq[b], s) : __fmaf_rn(t - qq[b], t - qq[b], s);
+                for (int b = 0; b < 16; b++) {
+                    const int t = (int)((wd[b >> 2] >> (8 * (b & 3))) & 0xffu), u = (int)qq[b];
+                    s += a.metric == SG_IP ? -t * u : (t - u) * (t - u);
+                }
+            }
+        } else {
+            const uint8_t* row = (const uint8_t*)a.x + (uint64_t)v * a.d;
+            for (uint32_t j = 0; j < a.d; j++) {
+                const int t = row[j], u = (int)qv[j];
+                s += a.metric == SG_IP ? -t * u : (t - u) * (t - u);
             }
         }
-    } else if (a.dtype == SG_U8) {
-        const uint8_t* row = (const uint8_t*)a.x + (uint64_t)v * a.d;
-        for (uint32_t j = 0; j < a.d; j++) {
-            const float t = (float)row[j];
-            s = a.metric == SG_IP ? __fmaf_rn(-t, qv[j], s) : __fmaf_rn(t - qv[j], t - qv[j], s);
-        }
-    } else if ((a.d & 3) == 0 && ((uintptr_t)a.x & 15) == 0) {
-        // 16-byte loads, same sequential fmaf order as the scalar loop (bit-identical result)
+        return (float)s;
+    }
+    // f32: fp64 products summed in index order, one rounding to f32 (no FMA contraction)
+    double s = 0.0;
+    if ((a.d & 3) == 0 && ((uintptr_t)a.x & 15) == 0) {
         const float4* row = (const float4*)((const float*)a.x + (uint64_t)v * a.d);
         for (uint32_t j4 = 0; j4 < (a.d >> 2); j4++) {
             const float4 t = __ldg(row + j4);
+            const float tt[4] = {t.x, t.y, t.z, t.w};
             const float* qq = qv + 4 * j4;
-            if (a.metric == SG_IP) {
-                s = __fmaf_rn(-t.x, qq[0], s); s = __fmaf_rn(-t.y, qq[1], s);
-                s = __fmaf_rn(-t.z, qq[2], s); s = __fmaf_rn(-t.w, qq[3], s);
-            } else {
-                s = __fmaf_rn(t.x - qq[0], t.x - qq[0], s); s = __fmaf_rn(t.y - qq[1], t.y - qq[1], s);
-                s = __fmaf_rn(t.z - qq[2], t.z - qq[2], s); s = __fmaf_rn(t.w - qq[3], t.w - qq[3], s);
+#pragma unroll
+            for (int b = 0; b < 4; b++) {
+                const double x = (double)tt[b], y = (double)qq[b];
+                s = a.metric == SG_IP ? __dsub_rn(s, __dmul_rn(x, y)) : __dadd_rn(s, __dmul_rn(x - y, x - y));
             }
         }
     } else {
         const float* row = (const float*)a.x + (uint64_t)v * a.d;
         for (uint32_t j = 0; j < a.d; j++) {
-            const float t = __ldg(row + j);
-            s = a.metric == SG_IP ? __fmaf_rn(-t, qv[j], s) : __fmaf_rn(t - qv[j], t - qv[j], s);
+            const double x = (double)__ldg(row + j), y = (double)qv[j];
+            s = a.metric == SG_IP ? __dsub_rn(s, __dmul_rn(x, y)) : __dadd_rn(s, __dmul_rn(x - y, x - y));
         }
     }
-    return s;
+    return (float)s;
+}
+
+// first visit of v? (marks it visited)
+__device__ __forceinline__ bool visit(const SearchArgs& a, uint32_t* vis, uint32_t v) {
+    if (!a.hash) {
+        const uint32_t bit = 1u << (v & 31);
+        return !(atomicOr(&vis[v >> 5], bit) & bit);
+    }
+    const uint32_t mask = (uint32_t)a.words - 1u;
+    uint32_t h = (v * 0x9E3779B1u) & mask;
+    for (uint32_t probe = 0; probe <= mask; probe++) {
+        const uint32_t old = atomicCAS(&vis[h], SG_SENT, v);
+        if (old == SG_SENT) return true;
+        if (old == v) return false;
+        h = (h + 1) & mask;
+    }
+    atomicExch(a.overflow, 1);
+    return false;
 }
 
 __device__ __forceinline__ uint32_t lower_bound_u64(const uint64_t* arr, uint32_t n, uint64_t key) {
@@ -85,7 +113,7 @@ __device__ __forceinline__ uint32_t lower_bound_u64(const uint64_t* arr, uint32_
 __global__ void __launch_bounds__(SW * 32) beam_kernel(SearchArgs a) {
     extern __shared__ __align__(16) uint8_t sm[];
     const uint32_t w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t per = (2 * a.poolcap + a.newcap) * 8 + 2 * a.poolcap * 4 + a.d * 4;
+    const uint32_t per = ((2 * a.poolcap + a.newcap) * 8 + 2 * a.poolcap * 4 + a.d * 4 + 15) & ~15u;   // 16-byte aligned
     uint8_t* base = sm + w * per;
     uint64_t* pool = (uint64_t*)base;
     uint64_t* pool2 = pool + a.poolcap;
@@ -99,14 +127,15 @@ __global__ void __launch_bounds__(SW * 32) beam_kernel(SearchArgs a) {
     for (uint32_t j = lane; j < a.d; j += 32)
         qv[j] = a.dtype == SG_U8 ? (float)((const uint8_t*)a.q)[(uint64_t)qi * a.d + j]
                                  : ((const float*)a.q)[(uint64_t)qi * a.d + j];
-    for (uint64_t i = lane; i < a.words; i += 32) vis[i] = 0;
+    const uint32_t clear = a.hash ? SG_SENT : 0u;
+    for (uint64_t i = lane; i < a.words; i += 32) vis[i] = clear;
     __syncwarp();
     __threadfence_block();
     unsigned long long nd = 1;
     if (lane == 0) {
         pool[0] = ((uint64_t)f2ord(qdist(a, qv, a.entry)) << 32) | a.entry;
         ex[0] = 0;
-        vis[a.entry >> 5] |= 1u << (a.entry & 31);
+        visit(a, vis, a.entry);
     }
     uint32_t np = 1;
     __syncwarp();
@@ -131,8 +160,7 @@ __global__ void __launch_bounds__(SW * 32) beam_kernel(SearchArgs a) {
             if (j < a.R) {
                 const uint32_t v = a.graph[(uint64_t)node * a.R + j];
                 if (v != SG_SENT) {
-                    const uint32_t bit = 1u << (v & 31);
-                    fresh = !(atomicOr(&vis[v >> 5], bit) & bit);
+                    fresh = visit(a, vis, v);
                     if (fresh) key = ((uint64_t)f2ord(qdist(a, qv, v)) << 32) | v;
                 }
             }
@@ -209,32 +237,47 @@ __global__ void shard_merge_kernel(const uint64_t* __restrict__ keys, uint32_t n
 
 static uint32_t pow2_at_least(uint32_t v) { uint32_t p = 32; while (p < v) p <<= 1; return p; }
 
-size_t beam_ws(uint64_t n, uint32_t nq) {
-    const uint64_t words = (n + 31) / 32;
+// visited-set words per query: the n-bit bitmap, or a hash set of 8 x beam x R slots when that
+// is smaller (large n); the second value says which
+static uint64_t vis_words(uint64_t n, uint32_t beam, uint32_t R, int* hash) {
+    const uint64_t bitmap = (n + 31) / 32;
+    uint64_t slots = 1024;
+    while (slots < 8ull * beam * R) slots <<= 1;
+    *hash = slots < bitmap;
+    return *hash ? slots : bitmap;
+}
+
+static uint64_t vis_batch(uint64_t words, uint32_t nq) {
     uint64_t batch = (1ull << 30) / (words * 4 + 1);
     if (batch < SW) batch = SW;
     if (batch > nq) batch = (nq + SW - 1) / SW * SW;
-    return batch * words * 4 + 4096;
+    return batch / SW * SW;
+}
+
+size_t beam_ws(uint64_t n, uint32_t nq, uint32_t beam, uint32_t R) {
+    int hash;
+    const uint64_t words = vis_words(n, beam, R, &hash);
+    return vis_batch(words, nq) * words * 4 + 4096 + 512;
 }
 
 sg_status beam_run(const void* x, sg_dtype dtype, uint64_t n, uint32_t d, const uint32_t* graph, uint32_t R,
                    uint32_t entry, const void* q, uint32_t nq, uint32_t topk, uint32_t beam, int metric,
                    uint32_t* out_ids, unsigned long long* ndist, Carver& cv, cudaStream_t st,
                    uint64_t* out_keys) {
-    const uint64_t words = (n + 31) / 32;
-    uint64_t batch = (1ull << 30) / (words * 4 + 1);
-    if (batch < SW) batch = SW;
-    if (batch > nq) batch = (nq + SW - 1) / SW * SW;
-    batch = batch / SW * SW;
+    int hash = 0;
+    const uint64_t words = vis_words(n, beam, R, &hash);
+    const uint64_t batch = vis_batch(words, nq);
     uint32_t* vis = cv.take<uint32_t>(batch * words);
+    int* overflow = cv.take<int>(1);
     if (!cv.ok()) { set_error("search: workspace too small"); return SG_ERR_WORKSPACE; }
+    SG_CUDA(cudaMemsetAsync(overflow, 0, sizeof(int), st));
     SearchArgs a{};
     a.x = x; a.q = q; a.graph = graph; a.visited = vis; a.out_ids = out_ids; a.out_keys = out_keys; a.n = n; a.words = words;
     a.d = d; a.R = R; a.entry = entry; a.nq = nq; a.topk = topk; a.beam = beam;
     a.poolcap = pow2_at_least(beam + R);
     a.newcap = pow2_at_least(R);
-    a.dtype = dtype; a.metric = metric; a.ndist = ndist;
-    const size_t per = (2 * a.poolcap + a.newcap) * 8 + 2 * a.poolcap * 4 + d * 4;
+    a.dtype = dtype; a.metric = metric; a.ndist = ndist; a.hash = hash; a.overflow = overflow;
+    const size_t per = ((2 * a.poolcap + a.newcap) * 8 + 2 * a.poolcap * 4 + d * 4 + 15) & ~(size_t)15;
     const size_t smem = per * SW;
     SG_CHECK_ARG(smem <= 200 * 1024, "search: beam/R/d too large for shared memory");
     SG_CUDA(cudaFuncSetAttribute(beam_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -243,6 +286,12 @@ sg_status beam_run(const void* x, sg_dtype dtype, uint64_t n, uint32_t d, const 
         const uint64_t cnt = batch < nq - q0 ? batch : nq - q0;
         beam_kernel<<<(unsigned)((cnt + SW - 1) / SW), SW * 32, smem, st>>>(a);
         SG_LAUNCHED("beam_kernel");
+    }
+    if (hash) {
+        int h = 0;
+        SG_CUDA(cudaMemcpyAsync(&h, overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
+        SG_CUDA(cudaStreamSynchronize(st));
+        if (h) { set_error("search: a visited hash set overflowed (8 x beam x R slots)"); return SG_ERR_WORKSPACE; }
     }
     return SG_OK;
 }

@@ -284,6 +284,47 @@ def test_search_u8_matches_oracle(api, oracle_mod, d):
     assert np.array_equal(u32(out), oo)
 
 
+@pytest.mark.parametrize("kind,d", [("gauss", 128), ("deep", 96), ("gauss", 25), ("u8", 25), ("u8", 99)])
+def test_search_exact_distances_match_oracle(api, oracle_mod, kind, d):
+    """P8 with exact distances on the GPU too (f32: fp64 sum of squared differences, one f32
+    rounding; u8: integers): result lists AND the distance-count proxy equal the
+    oracle's, on float data and on odd widths (unaligned rows)."""
+    if kind == "u8":
+        x, q = datagen.sift_like(2500, d, seed=71, as_u8=True), datagen.sift_like(80, d, seed=72, as_u8=True)
+    elif kind == "deep":
+        x, q = datagen.mixture(2500, d, 0.7, seed=71, normalise=True), datagen.mixture(80, d, 0.7, seed=72, normalise=True)
+    else:
+        x, q = datagen.gaussian(2500, d, seed=71), datagen.gaussian(80, d, seed=72)
+    ids, _ = oracle_mod.knn(x.numpy(), 16)
+    g = torch.from_numpy(ids.view(np.int32)).cuda()
+    out, _, _, nd = api.scalegann_search_eval(x.cuda(), g, 7, q.cuda(), topk=10, beam=24, return_ndist=True)
+    oo, od, ond = oracle_mod.search(x.numpy(), ids, 7, q.numpy(), topk=10, beam=24)
+    assert np.array_equal(u32(out), oo)
+    assert nd == int(ond.sum())
+
+
+def test_search_hash_visited_set_matches_oracle(api, oracle_mod):
+    """n = 70,000 with beam 16, R = 8: the visited set is the per-query hash set (1,024 slots
+    instead of a 2,188-word bitmap); the lists equal the oracle's."""
+    x = datagen.sift_like(70_000, 8, seed=73)
+    ids, _ = oracle_mod.knn(x.numpy(), 8)
+    q = datagen.sift_like(64, 8, seed=74)
+    out, _, _, nd = api.scalegann_search_eval(x.cuda(), torch.from_numpy(ids.view(np.int32)).cuda(), 0, q.cuda(),
+                                              topk=10, beam=16, return_ndist=True)
+    oo, _, ond = oracle_mod.search(x.numpy(), ids, 0, q.numpy(), topk=10, beam=16)
+    assert np.array_equal(u32(out), oo)
+    assert nd == int(ond.sum())
+
+
+def test_search_validation(api):
+    x = datagen.sift_like(500, 16, seed=75).cuda()
+    g = torch.zeros(500, 8, dtype=torch.int32, device="cuda")
+    with pytest.raises(ValueError):
+        api.scalegann_search_eval(x, g, 0, torch.zeros(4, 16, dtype=torch.uint8, device="cuda"))
+    with pytest.raises(ValueError):
+        api.scalegann_search_eval(x, g, 0, torch.zeros(4, 16))
+
+
 def test_search_shards_split_only_matches_oracle(api, oracle_mod):
     """Split-only build (k = 3, omega = 1) searched per shard with result merge (P:432-470,
     reading R15): GPU == oracle list for list; per-shard search beats one global beam."""
@@ -300,6 +341,10 @@ def test_search_shards_split_only_matches_oracle(api, oracle_mod):
     assert abs(rec - oracle_mod.recall(oo, ogt)) < 1e-12
     _, _, rec1 = api.scalegann_search_eval(x.cuda(), idx.merged, idx.entry, q.cuda(), topk=10, beam=32, gt=gt)
     assert rec > rec1
+    # an empty shard's SENTINEL entry (scalegann_entry_points) is skipped, not an error
+    out2, _, _ = api.scalegann_search_eval_shards(x.cuda(), idx.merged, list(entries) + [SENT], q.cuda(), topk=10,
+                                                  beam=32, gt=gt)
+    assert torch.equal(out2, out)
 
 
 # ------------------------------------------------------------------ a1 k-means
