@@ -35,7 +35,7 @@ def test_binding_covers_the_header():
 
 def test_abi_version_and_error_plumbing(lib):
     lib.scalegann_abi_version.restype = ctypes.c_int
-    assert lib.scalegann_abi_version() == 1
+    assert lib.scalegann_abi_version() == 2
     lib.scalegann_last_error.restype = ctypes.c_char_p
     # argument validation happens before any CUDA call: a null pointer is rejected on the host
     lib.scalegann_prune.restype = ctypes.c_int
