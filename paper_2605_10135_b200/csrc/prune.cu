@@ -7,6 +7,8 @@
 // increments cnt[r_ab] in shared memory.  The ranks are then ordered stably by (cnt, rank)
 // (sentinel ranks last) with a counting sort and the first R written with their kNN distances.
 // Bit-exact with the oracle (integer work only).
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace sg {
@@ -45,19 +47,58 @@ __device__ __forceinline__ uint32_t lookup(const uint4* bk, const uint2* br, con
 
 constexpr uint32_t QCAP = 256;   // lookup queue entries per warp (flushed every 256 / (32 LPL) rows)
 
+// 2-hop rows r0..r0+3 of N[a]: lane holds ids [LPL lane, LPL lane + LPL) of each row (r_db =
+// LPL lane + q), one vector load per row when the rows are full (L = 32 LPL)
 template <int LPL>
 __device__ __forceinline__ void load_rows(const uint32_t* __restrict__ knn, const uint32_t* na, uint32_t r0, uint32_t L,
                                           uint32_t lane, uint32_t (&bv)[4][LPL]) {
 #pragma unroll
     for (int u = 0; u < 4; u++) {
         const uint32_t dl = r0 + u < L ? na[r0 + u] : SG_SENT;
+        const uint32_t* row = knn + (uint64_t)dl * L + LPL * lane;
+        bool done = false;
+        if (dl == SG_SENT) {
 #pragma unroll
-        for (int q = 0; q < LPL; q++) {
-            const uint32_t rdb = q * 32 + lane;
-            bv[u][q] = (dl != SG_SENT && rdb < L) ? __ldg(knn + (uint64_t)dl * L + rdb) : SG_SENT;
+            for (int q = 0; q < LPL; q++) bv[u][q] = SG_SENT;
+            done = true;
+        } else if (L == 32 * LPL) {
+            if constexpr (LPL == 4) {
+                const uint4 v = __ldg((const uint4*)row);
+                bv[u][0] = v.x; bv[u][1] = v.y; bv[u][2] = v.z; bv[u][3] = v.w;
+                done = true;
+            } else if constexpr (LPL == 2) {
+                const uint2 v = __ldg((const uint2*)row);
+                bv[u][0] = v.x; bv[u][1] = v.y;
+                done = true;
+            }
+        }
+        if (!done) {
+#pragma unroll
+            for (int q = 0; q < LPL; q++) bv[u][q] = LPL * lane + q < L ? __ldg(row + q) : SG_SENT;
         }
     }
 }
+
+// per-warp shared-memory layout (byte offsets, 16-byte aligned pieces)
+template <int LPL>
+struct PruneLayout {
+    static constexpr uint32_t LP = LPL * 32, NB = LP / 2;
+    static constexpr int FLUSH = QCAP / (32 * LPL) < 4 ? QCAP / (32 * LPL) : 4;
+    static constexpr uint32_t al(size_t v) { return (uint32_t)((v + 15) / 16 * 16); }
+    static constexpr uint32_t BKEYS = 0;
+    static constexpr uint32_t BRANKS = al(BKEYS + NB * 32);
+    static constexpr uint32_t BFILL = al(BRANKS + NB * 8);
+    static constexpr uint32_t SK = al(BFILL + NB * 4);
+    static constexpr uint32_t SR = al(SK + STASH * 4);
+    static constexpr uint32_t NST = al(SR + STASH);
+    static constexpr uint32_t BLOOM = al(NST + 16);
+    static constexpr uint32_t CNT = al(BLOOM + 128);
+    static constexpr uint32_t NA = al(CNT + LP * 4);
+    static constexpr uint32_t OFF = al(NA + LP * 4);
+    static constexpr uint32_t STG = al(OFF + (LP + 1) * 4);
+    static constexpr uint32_t QE = al(STG + 32 * FLUSH * LPL * 4);
+    static constexpr uint32_t PER = al(QE + QCAP * 8);
+};
 
 template <int LPL, int PW, int RULE>   // ranks per lane = L_pad / 32; warps (nodes) per CTA; prune rule
 __global__ void __launch_bounds__(PW * 32) prune_kernel(const uint32_t* __restrict__ knn, const float* __restrict__ knn_d,
@@ -66,24 +107,25 @@ __global__ void __launch_bounds__(PW * 32) prune_kernel(const uint32_t* __restri
     constexpr uint32_t LP = LPL * 32;          // padded L (power of two)
     constexpr uint32_t NB = LP / 2;            // buckets of 8 slots: load factor 1/4
     constexpr uint32_t NBB = LPL == 1 ? 4 : LPL == 2 ? 5 : LPL == 4 ? 6 : 7;
-    constexpr int FLUSH = QCAP / (32 * LPL) < 4 ? QCAP / (32 * LPL) : 4;   // rows per queue flush
+    constexpr int FLUSH = PruneLayout<LPL>::FLUSH;   // rows per queue flush
     static_assert((1u << NBB) == NB, "bucket bits");
     extern __shared__ __align__(16) uint8_t sm[];
     const uint32_t w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
-    constexpr size_t PER = NB * 32 + NB * 8 + NB * 4 + STASH * 4 + STASH + 16 + 128 + LP * 4 * 2 + (LP + 1) * 4 + 8 + QCAP * 8;
-    uint8_t* base = sm + (size_t)w * ((PER + 15) / 16 * 16);
-    uint32_t* bkeys = (uint32_t*)base;                 // [NB][8]
-    uint8_t* branks = base + NB * 32;                  // [NB][8]
-    uint32_t* bfill = (uint32_t*)(branks + NB * 8);    // [NB]
-    uint32_t* sk = bfill + NB;                         // stash keys
-    uint8_t* sr = (uint8_t*)(sk + STASH);              // stash ranks
-    uint32_t* nst = (uint32_t*)(((uintptr_t)(sr + STASH) + 15) & ~(uintptr_t)15);   // stash count
-    uint32_t* bloom = nst + 4;                         // 32 words
-    uint32_t* cnt = bloom + 32;                        // detour count per rank
-    uint32_t* na = cnt + LP;                           // N[a]
-    uint32_t* off = na + LP;                           // counting-sort offsets per count value (L + 1)
-    uint64_t* qe = (uint64_t*)(((uintptr_t)(off + LP + 1) + 7) & ~(uintptr_t)7);   // queue: max(r_ad, r_db) << 32 | id
+    using Lay = PruneLayout<LPL>;
+    uint8_t* base = sm + (size_t)w * Lay::PER;
+    uint32_t* bkeys = (uint32_t*)(base + Lay::BKEYS);  // [NB][8]
+    uint8_t* branks = base + Lay::BRANKS;              // [NB][8]
+    uint32_t* bfill = (uint32_t*)(base + Lay::BFILL);  // [NB]
+    uint32_t* sk = (uint32_t*)(base + Lay::SK);        // stash keys
+    uint8_t* sr = base + Lay::SR;                      // stash ranks
+    uint32_t* nst = (uint32_t*)(base + Lay::NST);      // stash count
+    uint32_t* bloom = (uint32_t*)(base + Lay::BLOOM);  // 32 words
+    uint32_t* cnt = (uint32_t*)(base + Lay::CNT);      // detour count per rank
+    uint32_t* na = (uint32_t*)(base + Lay::NA);        // N[a]
+    uint32_t* off = (uint32_t*)(base + Lay::OFF);      // counting-sort offsets per count value (L + 1)
+    uint32_t* stg = (uint32_t*)(base + Lay::STG);      // per lane: the 2-hop ids of one flush group
+    uint64_t* qe = (uint64_t*)(base + Lay::QE);        // queue: max(r_ad, r_db) << 32 | id
     const uint64_t nwarps = (uint64_t)gridDim.x * PW;
     for (uint64_t a = (uint64_t)blockIdx.x * PW + w; a < m; a += nwarps) {
         const uint32_t* Na = knn + a * L;
@@ -133,7 +175,8 @@ __global__ void __launch_bounds__(PW * 32) prune_kernel(const uint32_t* __restri
                 if (r0 + 4 < L) load_rows<LPL>(knn, na, r0 + 4, L, lane, bn);
 #pragma unroll
                 for (int u0 = 0; u0 < 4; u0 += FLUSH) {
-                    // (1) filter FLUSH rows x LPL ids per lane into a local bit mask
+                    // (1) filter FLUSH rows x LPL ids per lane into a local bit mask (slot u * LPL + q);
+                    //     SENT and a itself are never in the table, so they need no special case
                     uint32_t lm = 0;
 #pragma unroll
                     for (int u = u0; u < u0 + FLUSH; u++)
@@ -142,8 +185,10 @@ __global__ void __launch_bounds__(PW * 32) prune_kernel(const uint32_t* __restri
                             const uint32_t b = bv[u][q];
                             const uint32_t fw = __shfl_sync(0xffffffffu, fword, (b >> 5) & 31u);
                             lm |= (__funnelshift_r(fw, fw, b) & 1u) << ((u - u0) * LPL + q);
+                            stg[((u - u0) * LPL + q) * 32 + lane] = b;   // slot-major: conflict free
                         }
                     // (2) queue offsets: exclusive warp scan of the positives per lane
+                    if (rule & 0x200u) lm = 0;   // diagnostics ablation: no queue
                     const uint32_t np = __popc(lm);
                     uint32_t inc = np;
 #pragma unroll
@@ -153,20 +198,19 @@ __global__ void __launch_bounds__(PW * 32) prune_kernel(const uint32_t* __restri
                     }
                     const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
                     uint32_t pos = inc - np;
-                    // (3) append (max(r_ad, r_db) << 32 | id) of the positives, fixed order
-#pragma unroll
-                    for (int u = u0; u < u0 + FLUSH; u++)
-#pragma unroll
-                        for (int q = 0; q < LPL; q++)
-                            if ((lm >> ((u - u0) * LPL + q)) & 1u) {
-                                // only ranks r_ab > max(r_ad, r_db) (rule P) / > r_ad (rule 1) count
-                                const uint32_t r_ad = r0 + u, r_db = q * 32 + lane;
-                                const uint32_t mx = RULE == 0 ? max(r_ad, r_db) : r_ad;
-                                qe[pos++] = ((uint64_t)mx << 32) | bv[u][q];
-                            }
+                    // (3) append (max(r_ad, r_db) << 32 | id) of the positives only (loop over the
+                    //     set bits; the ids come back from the lane's staging slots)
+                    while (lm) {
+                        const uint32_t j = __ffs(lm) - 1;
+                        lm &= lm - 1;
+                        const uint32_t r_ad = r0 + u0 + j / LPL, r_db = LPL * lane + j % LPL;
+                        // only ranks r_ab > max(r_ad, r_db) (rule P) / > r_ad (rule 1) count
+                        const uint32_t mx = RULE == 0 ? max(r_ad, r_db) : r_ad;
+                        qe[pos++] = ((uint64_t)mx << 32) | stg[j * 32 + lane];
+                    }
                     __syncwarp();
                     // (4) resolve the queue densely against the table
-                    for (uint32_t i = lane; i < total; i += 32) {
+                    for (uint32_t i = lane; i < ((rule & 0x100u) ? 0u : total); i += 32) {   // 0x100: no lookups
                         const uint64_t e = qe[i];
                         const uint32_t b = (uint32_t)e;
                         const uint32_t r_ab = lookup<NB, NBB>((const uint4*)bkeys, (const uint2*)branks, sk, sr, nstash, b);
@@ -227,9 +271,7 @@ __global__ void __launch_bounds__(PW * 32) prune_kernel(const uint32_t* __restri
 
 template <int LPL, int PW>
 size_t prune_smem() {
-    constexpr uint32_t LP = LPL * 32, NB = LP / 2;
-    constexpr size_t PER = NB * 32 + NB * 8 + NB * 4 + STASH * 4 + STASH + 16 + 128 + LP * 4 * 2 + (LP + 1) * 4 + 8 + QCAP * 8;
-    return (size_t)PW * ((PER + 15) / 16 * 16) + 64;
+    return (size_t)PW * PruneLayout<LPL>::PER + 64;
 }
 
 template <int LPL, int PW, int RULE>
@@ -252,17 +294,20 @@ sg_status prune_launch(const uint32_t* knn, const float* knn_d, uint64_t m, uint
 
 sg_status launch_prune(const uint32_t* knn, const float* knn_d, uint64_t m, uint32_t L, uint32_t R, uint32_t rule,
                        uint32_t* out, float* out_d, cudaStream_t st) {
+    static int abl = -1;   // diagnostics: SG_PRUNE_ABL bit 0 skips the table lookups, bit 1 the queue
+    if (abl < 0) { const char* e = getenv("SG_PRUNE_ABL"); abl = e ? atoi(e) : 0; }
+    const uint32_t rl = rule | ((uint32_t)abl << 8);
     if (m == 0) return SG_OK;
     if (rule == 0) {
-        if (L <= 32) return prune_launch<1, 8, 0>(knn, knn_d, m, L, R, rule, out, out_d, st);
-        if (L <= 64) return prune_launch<2, 8, 0>(knn, knn_d, m, L, R, rule, out, out_d, st);
-        if (L <= 128) return prune_launch<4, 8, 0>(knn, knn_d, m, L, R, rule, out, out_d, st);
-        return prune_launch<8, 4, 0>(knn, knn_d, m, L, R, rule, out, out_d, st);
+        if (L <= 32) return prune_launch<1, 8, 0>(knn, knn_d, m, L, R, rl, out, out_d, st);
+        if (L <= 64) return prune_launch<2, 8, 0>(knn, knn_d, m, L, R, rl, out, out_d, st);
+        if (L <= 128) return prune_launch<4, 8, 0>(knn, knn_d, m, L, R, rl, out, out_d, st);
+        return prune_launch<8, 4, 0>(knn, knn_d, m, L, R, rl, out, out_d, st);
     }
-    if (L <= 32) return prune_launch<1, 8, 1>(knn, knn_d, m, L, R, rule, out, out_d, st);
-    if (L <= 64) return prune_launch<2, 8, 1>(knn, knn_d, m, L, R, rule, out, out_d, st);
-    if (L <= 128) return prune_launch<4, 8, 1>(knn, knn_d, m, L, R, rule, out, out_d, st);
-    return prune_launch<8, 4, 1>(knn, knn_d, m, L, R, rule, out, out_d, st);
+    if (L <= 32) return prune_launch<1, 8, 1>(knn, knn_d, m, L, R, rl, out, out_d, st);
+    if (L <= 64) return prune_launch<2, 8, 1>(knn, knn_d, m, L, R, rl, out, out_d, st);
+    if (L <= 128) return prune_launch<4, 8, 1>(knn, knn_d, m, L, R, rl, out, out_d, st);
+    return prune_launch<8, 4, 1>(knn, knn_d, m, L, R, rl, out, out_d, st);
 }
 
 }  // namespace sg
