@@ -352,7 +352,7 @@ def main():
     owned = [s for s in range(k) if idx.owner[s] == rank]
     alg_flops_step = sum(2.0 * idx.sizes[s] ** 2 * d for s in owned)
     peaks, src = load_peaks()
-    prec_is_f16 = kind in ("sift", "sift_u8")   # integer data -> F16_EXACT (AUTO); float -> TF32 at half rate
+    prec_is_f16 = kind in ("sift", "sift_u8")   # integer data -> F16_EXACT (AUTO); float -> 3xTF32 (AUTO)
     peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")) * (1.0 if prec_is_f16 else 0.5)
     achieved = alg_flops_step * args.steps / (knn_ms / 1000.0) / 1e12 if knn_ms > 0 else None
     traffic, pipe_pct, prof_src = None, None, None
@@ -370,6 +370,7 @@ def main():
                 "ncu_tensor_pipe_active_pct": pipe_pct, "ncu_source": prof_src,
                 "kernel": "knn_tc_kernel (tcgen05.mma kind::%s, fp32 accumulate)" % ("f16" if prec_is_f16 else "tf32"),
                 "peak_source": f"{src} bf16 dense sustained" + (" (f16 = bf16 rate)" if prec_is_f16 else " x 0.5 (tf32)"),
+                "tensor_work_per_algorithmic_flop": 1 if prec_is_f16 else 3,
                 "per_unit": f"2*d flops per (row, column) pair; m_s^2 pairs per shard launch (d = {d})",
                 "knn_ms_per_step": knn_ms / args.steps, "knn_launches": knn_launches,
                 "knn_share_of_step": (knn_ms / args.steps) / (ms / args.steps)}
@@ -446,10 +447,10 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": scaling,
-            "vs_baseline": None, "dtype": "f16" if prec_is_f16 else "tf32", "data": "synthetic",
+            "vs_baseline": None, "dtype": "f16" if prec_is_f16 else "tf32x3", "data": "synthetic",
             "config": {"workload": wl, "n": n, "d": d, "k": k, "omega": 2, "epsilon": 1.2, "L": 128, "R": 64,
                        "precision": ("F16_EXACT operands, fp32 accumulate (exact for this integer data)"
-                                     if prec_is_f16 else "TF32 operands (AUTO), fp32 accumulate"),
+                                     if prec_is_f16 else "3xTF32 operands (AUTO: hi/lo split, ~fp32 products), fp32 accumulate"),
                        "shard_sizes": idx.sizes, "replicas": sum(idx.counts["repl"]),
                        "l2": f"inputs ({n * d * elem / 1e6:.0f} MB/rank) larger than the 126 MB L2; no explicit flush",
                        "parallelism": f"shard-parallel x{world} (LPT on m^2), library NCCL bcast + send/recv"},

@@ -55,7 +55,7 @@ typedef enum { SG_L2 = 0, SG_IP = 1 } sg_metric;   /* squared L2 / negative inne
 
 /* Operand precision of the distance GEMM; accumulation is always fp32 (R3). */
 typedef enum {
-    SG_PREC_AUTO = 0,       /* F16_EXACT when exact (u8, or integral f32 with the bound below), else TF32 */
+    SG_PREC_AUTO = 0,       /* F16_EXACT when exact (u8, or integral f32 with the bound below), else TF32X3 */
     SG_PREC_F16_EXACT = 1,  /* kind::f16; exact when all values are integers |v| <= 2048 and 2*d*max^2 < 2^24 */
     SG_PREC_TF32 = 2,       /* kind::tf32, operands rounded to tf32 (RN) */
     SG_PREC_TF32X3 = 3      /* kind::tf32 on [hi|hi|lo].[hi|lo|hi]: ~fp32-accurate products */

@@ -108,7 +108,7 @@ static int worst_prec(sg_dtype dtype, int32_t precision, uint32_t d) {
     // F16_EXACT whenever 2 d 255^2 < 2^24 (gather.cu resolves it without looking at the data)
     if (precision != SG_PREC_AUTO) return precision;
     if (dtype == SG_U8 && 2ull * d * 255 * 255 < (1ull << 24)) return SG_PREC_F16_EXACT;
-    return SG_PREC_TF32;
+    return dtype == SG_U8 ? SG_PREC_TF32 : SG_PREC_TF32X3;
 }
 
 static sg_status check_knn_shape(int prec, int metric, uint32_t d, uint32_t L) {

@@ -99,3 +99,18 @@ def test_knn_40k_rows_f32_tolerance(oracle_mod, tmp_path, prec, mode):
     assert all(r not in gi[r] for r in rows)    # no self loops
     fails, first = check_knn(gi[rows], gd[rows], oi, od, x[rows], x, self_exclude=False)
     assert fails == 0, f"{fails} of {len(rows)} rows fail the P4 checker: {first}"
+
+
+@pytest.mark.parametrize("prec", [0, 3])
+def test_knn_c2_density_f32_p4_checker(oracle_mod, tmp_path, prec):
+    """C2-shaped density (DEEP-like 96-d L2-normalised, 200,000 rows): 2,000
+    sampled rows pass the P4 checker with AUTO (which must pick an accurate enough precision for
+    non-integer data) and with TF32X3."""
+    m, L, seed = 200_000, 128, 35
+    gi, gd, log = _run(tmp_path, {}, m, L, seed, "deep", prec)
+    x = datagen.mixture(m, 96, 0.7, seed=seed, normalise=True).numpy()
+    rng = np.random.default_rng(seed)
+    rows = np.array(sorted(rng.choice(m, size=2000, replace=False).tolist()), np.int64)
+    oi, od = oracle_rows(oracle_mod, x, rows, L)
+    fails, first = check_knn(gi[rows], gd[rows], oi, od, x[rows], x, self_exclude=False)
+    assert fails == 0, f"precision {prec}: {fails} of {len(rows)} rows fail the P4 checker: {first}"
