@@ -18,14 +18,19 @@
 //           128 columns, 2 x 2 = all 512 columns, so a tile's MMAs overlap the previous drain.
 //   warps 2..17: epilogue in two column streams (columns [64 s, 64 s + 64) of every tile);
 //           warp (q, a, s) owns rows a*128 + q*32 + lane (TMEM lane quadrant q of half a).  Per
-//           32-column pass a thread (= one row) builds the pass mask with FADD2 + funnel shifts
-//           (sign of key - next_up(thr): 1.5 instructions per key) and appends only set bits, as
-//           (key bits << 32 | id), to its (row, stream) buffer (global, L2 resident).  A buffer
-//           that fills is compacted by ballot-count bit descent (select_pairs); the row threshold
-//           is one (key, id) pair in shared memory shared by both streams (atomicMin).  Thresholds
-//           are extrapolated from the fraction of columns seen (R15); the final phase checks each
-//           row (>= L union entries at or below the pair), selects and sorts its top-L, and lists
-//           the rows that fail for the fallback launch (rank-L thresholds).
+//           32-column pass a thread (= one row) takes the minimum of its 32 keys (16 FMNMX3) and
+//           compares it with its row threshold; only the rows that pass (a few % after the first
+//           tiles) stage their keys in shared memory, and the warp then takes those rows one at
+//           a time, lane j testing column j: one ballot per row, the passing
+//           (key bits << 32 | id) words appended to consecutive slots of the row's (row, stream)
+//           buffer (global, L2 resident).  Both passes of a tile are loaded (and the TMEM
+//           buffer handed back to the MMA) before any insertion or compaction.  A buffer above
+//           its trigger is compacted by ballot-count bit descent (select_pairs); the row
+//           threshold is one (key, id) pair in shared memory shared by both streams (atomicMin).
+//           The self column is inserted like any other and removed in the final phase.
+//           Thresholds are extrapolated from the fraction of columns seen (I1); the final phase
+//           checks each row (>= L union entries at or below the pair), selects and sorts its
+//           top-L, and lists the rows that fail for the fallback launch (rank-L thresholds).
 #include "knn_common.cuh"
 
 namespace sg {

@@ -242,7 +242,7 @@ knn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         // ===================== epilogue (both CTAs): fused selection, four column streams =====
         // Same rules as knn_tc.cu: inclusive insertion test against the row's shared (key, id)
         // pair, prefilter per 32-column pass, per-row insertion by one ballot, compaction by bit
-        // descent, extrapolated thresholds (R15) checked per row at the end, self column removed
+        // descent, extrapolated thresholds (I1) checked per row at the end, self column removed
         // in the final phase.
         const uint32_t e = warp - 2, s = e >> 2, q = warp & 3;
         const uint32_t r = q * 32 + lane;                    // row within the CTA's 128
