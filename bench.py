@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--e2e", action="store_true", help="C2-C4: also time the host-buffer e2e leg")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-recall", action="store_true")
+    ap.add_argument("--no-stages", action="store_true", help="skip the extra untimed step of the stage breakdown")
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle parity check at bench size")
     ap.add_argument("--profile-steps", action="store_true", help="minimal run for ncu (no e2e/cpu/recall)")
     return ap.parse_args()
@@ -410,7 +411,7 @@ def main():
         del xh
 
     # ---------------- per-stage breakdown from one extra (untimed) step
-    stage_ms = build_index(x, cfg, rank, world, comm, timing=True).stage_ms
+    stage_ms = None if args.no_stages else build_index(x, cfg, rank, world, comm, timing=True).stage_ms
 
     # ---------------- recall@10 of the merged graph (untimed evaluation, a9)
     recall = None
