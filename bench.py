@@ -20,6 +20,8 @@ from __future__ import annotations
 import argparse
 import json
 import os
+
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")   # big configs: no fragmentation
 import statistics
 import subprocess
 import sys
@@ -319,7 +321,9 @@ def main():
     def step(inp):
         return build_index(inp, cfg, rank, world, comm)
 
+    idx = None
     for _ in range(args.warmup):
+        idx = None   # one index alive at a time (C4 at N = 1: 51 GB of merged rows each)
         idx = step(x)
     torch.cuda.synchronize()
     barrier()
@@ -335,6 +339,7 @@ def main():
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record()
     for _ in range(args.steps):
+        idx = None
         idx = step(x)
     t1.record()
     torch.cuda.synchronize()

@@ -163,6 +163,7 @@ class Workspace:
     def get(self, nbytes: int) -> torch.Tensor:
         nbytes = max(int(nbytes), 256)
         if self.buf is None or self.buf.numel() < nbytes:
+            self.buf = None   # release the smaller buffer before the larger one is allocated
             self.buf = torch.empty(nbytes, dtype=torch.uint8, device=self.device or "cuda")
         return self.buf
 
