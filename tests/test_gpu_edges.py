@@ -59,8 +59,8 @@ def test_prune_reverse_sentinel_padded(api, oracle_mod, m, L, R):
     assert np.array_equal(u32(g), f) and np.array_equal(gd.cpu().numpy(), fd)
 
 
-def _oracle_graph(oracle_mod, x, C, cfg):
-    r = oracle_mod.partition(x, C, omega=cfg.omega, eps=cfg.epsilon, block_size=cfg.block_size)
+def _oracle_graph(oracle_mod, x, C, cfg, capacity=0):
+    r = oracle_mod.partition(x, C, omega=cfg.omega, eps=cfg.epsilon, block_size=cfg.block_size, capacity=capacity)
     idm, gs, gds = [], [], []
     for s in range(cfg.k):
         im = oracle_mod.idmap(r["home"], s)
@@ -91,8 +91,9 @@ def test_empty_shard(api, oracle_mod):
     x = datagen.sift_like(4000, 64, seed=85)
     C = torch.cat([x[::2000][:2], torch.full((1, 64), 1e6)]).contiguous()
     cfg = BuildConfig(k=3, omega=2, L=32, R=16, block_size=1024)
+    # capacity 4000: the two near clusters never fill, so no primary spills to the far one
     home, pd, counts = api.scalegann_partition(x.cuda(), C.cuda(), omega=2, epsilon=cfg.epsilon,
-                                               block_size=cfg.block_size)
+                                               block_size=cfg.block_size, capacity=4000)
     assert counts["sizes"][2] == 0
     idm, gs, gds = [], [], []
     for s in range(3):
@@ -103,7 +104,7 @@ def test_empty_shard(api, oracle_mod):
         g, gd = api.scalegann_build_shard(x.cuda(), idm[-1], cfg.L, cfg.R)
         gs.append(g), gds.append(gd)
     merged, merged_d = api.scalegann_merge(home, idm, gs, gds)
-    r, (om, omd) = _oracle_graph(oracle_mod, x.numpy(), C.numpy(), cfg)
+    r, (om, omd) = _oracle_graph(oracle_mod, x.numpy(), C.numpy(), cfg, capacity=4000)
     assert np.array_equal(u32(home), r["home"])
     assert np.array_equal(u32(merged), om) and np.array_equal(merged_d.cpu().numpy(), omd)
     g, per = api.scalegann_entry_points(home, pd, counts["sizes"])
