@@ -43,6 +43,19 @@ void knn_time_begin(cudaStream_t st);
 void knn_time_end(cudaStream_t st);
 }  // namespace sg
 
+// Device-side invariant checks of the debug build (SG_NVCC_FLAGS=-DSG_DEBUG_CHECKS=1): a violated
+// bound traps the kernel (the launch then fails loudly); compiled out of the production build.
+#if defined(SG_DEBUG_CHECKS) && SG_DEBUG_CHECKS
+#define SG_DCHECK(cond)          \
+    do {                         \
+        if (!(cond)) __trap();   \
+    } while (0)
+#else
+#define SG_DCHECK(cond) \
+    do {                \
+    } while (0)
+#endif
+
 #define SG_TRY(call)                              \
     do {                                          \
         sg_status _s = (call);                    \

@@ -314,6 +314,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     __syncwarp();
                     cnt += insert_rows(p, skeys, lane, hb1, cb + 32, pw);
                 }
+                SG_DCHECK(cnt <= C);   // a tile's two passes fit the ROOM above the trigger
                 c0 = clk();
                 pw[4] += c0 - c1;
                 // make room for the next tile (<= ROOM more entries): compact rows whose buffer
@@ -334,6 +335,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                         uint64_t P = select_pairs<EPL>(ob, c_o, cap, want, kmax, lane, &kept);
                         if (kept > C - ROOM)   // massive ties on the threshold key: split them by id
                             P = select_L<EPL>(ob, kept, want, kmax, hist, lane, &kept);
+                        SG_DCHECK(kept <= C - ROOM);
                         if (lane == (uint32_t)o) {
                             cnt = kept;
                             atomicMin(&s_pair[R], (unsigned long long)P);

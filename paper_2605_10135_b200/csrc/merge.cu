@@ -168,6 +168,7 @@ __device__ void fold_row(uint32_t* __restrict__ mrow, float* __restrict__ mrow_d
         a2 += __popc(bal);
         __syncwarp();
     }
+    SG_DCHECK(a <= R && b <= R && a2 <= a);
     // sort B (bitonic over the next power of two)
     uint32_t np = 32;
     while (np < b) np <<= 1;
@@ -213,6 +214,7 @@ __global__ void __launch_bounds__(MW * 32) merge_shard_kernel(
         const float* grow_d = graph_d + l * R;
         if (o.owner[home[g * omega]] == rank) {
             const uint64_t oi = owned_index[g];
+            SG_DCHECK(oi != SG_SENT);
             uint32_t* mrow = merged + oi * R;
             float* mrow_d = merged_d + oi * R;
             if (nh == 1) {   // single home: the shard row as is
@@ -230,6 +232,7 @@ __global__ void __launch_bounds__(MW * 32) merge_shard_kernel(
                 fold_row(mrow, mrow_d, s_id[w], grow_d, R, s_f[w], lane);
             }
         } else {   // primary owned elsewhere: a record for its owner
+            SG_DCHECK(rec_slot[g * omega + h] != SG_SENT);
             uint32_t* r = sendbuf + (uint64_t)rec_slot[g * omega + h] * W;
             if (lane == 0) { r[0] = (uint32_t)g; r[1] = h; }
             for (uint32_t j = lane; j < R; j += 32) {

@@ -197,6 +197,7 @@ __global__ void __launch_bounds__(PW * 32) prune_kernel(const uint32_t* __restri
                         if (lane >= (uint32_t)o) inc += t;
                     }
                     const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+                    SG_DCHECK(total <= QCAP);
                     uint32_t pos = inc - np;
                     // (3) append (max(r_ad, r_db) << 32 | id) of the positives only (loop over the
                     //     set bits; the ids come back from the lane's staging slots)

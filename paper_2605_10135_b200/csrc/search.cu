@@ -168,6 +168,7 @@ __global__ void __launch_bounds__(SW * 32) beam_kernel(SearchArgs a) {
             if (fresh) nb[nn + __popc(bal & ((1u << lane) - 1u))] = key;
             nn += __popc(bal);
         }
+        SG_DCHECK(nn <= a.newcap && np <= a.beam);
         nd += nn;
         if (nn == 0) { __syncwarp(); continue; }
         uint32_t p2 = 32;
