@@ -16,3 +16,7 @@ python tools/profile_knn.py --m $M --reps 1 > /dev/null 2>&1 && \
 ncu --set full --import-source on --clock-control none -k regex:knn_tc -s 0 -c 1 -f -o gpurun_out/${TAG}_knn_full \
     python tools/profile_knn.py --m $M --reps 1 > gpurun_out/${TAG}_knn_full.log 2>&1
 echo "ncu full rc=$?"
+python tools/profile_build.py --m 450000 --reps 1 > /dev/null 2>&1 && \
+ncu --set full --import-source on --clock-control none -k regex:"prune_kernel|reverse_merge|scatter_kernel|indeg_kernel" -c 4 -f \
+    -o gpurun_out/prune_full python tools/profile_build.py --m 450000 --reps 1 > gpurun_out/${TAG}_prune_full.log 2>&1
+echo "ncu prune rc=$?"

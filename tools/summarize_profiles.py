@@ -92,7 +92,7 @@ def main():
             per_node = 67328 if "prune" in name else 1920
             alg = 450000 * per_node / (ms / 1e3) / 1e9
             out.append(f"{name}: {ms:.3f} ms, algorithmic {alg:.0f} GB/s "
-                       f"({100 * alg / 6557.8:.1f}% of 6557.8 GB/s measured HBM)")
+                       f"({100 * alg / 6550.4:.1f}% of 6550.4 GB/s measured HBM)")
             for k in ["dram__bytes_read.sum", "dram__bytes_write.sum", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
                       "lts__t_bytes.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
                       "sm__inst_executed.avg.per_cycle_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
