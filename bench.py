@@ -381,28 +381,29 @@ def main():
                 "knn_ms_per_step": knn_ms / args.steps, "knn_launches": knn_launches,
                 "knn_share_of_step": (knn_ms / args.steps) / (ms / args.steps)}
 
-    # ---------------- e2e through the public API with host buffers
+    # ---------------- e2e through the C ABI with HOST buffers (scalegann_build_index_host: the
+    # dataset copied to the device, a1-a8, the owned merged rows copied back, in one call per step)
     e2e = None
     if not args.no_e2e:
-        # every rank copies the whole dataset host -> device (the partition runs on every rank,
-        # no dataset collective) and reads back the merged rows it owns
         xh = x.cpu().pin_memory()
-        outh = torch.empty(tuple(idx.merged.shape), dtype=idx.merged.dtype, pin_memory=True)
+        outh = torch.empty(n * cfg.R, dtype=torch.int32, pin_memory=True)
         h2d = xh.numel() * elem * world
-        d2h_local = outh.numel() * outh.element_size()
+        kw = dict(k=cfg.k, omega=cfg.omega, epsilon=cfg.epsilon, theta0_ppm=cfg.theta0_ppm, alpha=cfg.alpha,
+                  block_size=cfg.block_size, L_=cfg.L, R=cfg.R, kmeans_seed=cfg.kmeans_seed)
+        idx = None   # the device-timed index is not needed any more (C4 memory)
+        api.scalegann_build_index_host(xh, outh, comm, **kw)   # warm-up (stream-ordered pool)
         barrier()
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(args.steps):
-            xd = xh.to("cuda", non_blocking=True)
-            ix = step(xd)
-            outh.copy_(ix.merged, non_blocking=True)
+            n_owned, _ = api.scalegann_build_index_host(xh, outh, comm, **kw)
         e1.record()
         torch.cuda.synchronize()
         barrier()
         ems = e0.elapsed_time(e1)
+        d2h_local = n_owned * cfg.R * 4
         d2h = d2h_local
         if world > 1:
             tt = torch.tensor([ems, float(d2h_local)], dtype=torch.float64, device="cuda")
@@ -412,8 +413,10 @@ def main():
             ems, d2h = float(t_max[0].item()), int(tt[1].item())
         e2e = {"value": n * args.steps / (ems / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": ems / args.steps,
+               "api": "scalegann_build_index_host (one C-ABI call per step, host buffers in and out)",
                "note": "whole-job bytes: the full dataset to every rank, each rank's owned merged rows back"}
-        del xh
+        del xh, outh
+        idx = step(x)   # the device index again, for the legs below
 
     # ---------------- per-stage breakdown from one extra (untimed) step
     stage_ms = None if args.no_stages else build_index(x, cfg, rank, world, comm, timing=True).stage_ms

@@ -248,6 +248,21 @@ sg_status scalegann_merge(void* comm, const uint32_t* home, uint64_t n, uint32_t
                           const float* const* graphs_d, uint32_t R, uint32_t* merged, float* merged_d,
                           uint64_t* n_owned_host, void* ws, size_t ws_bytes, void* stream);
 
+/* ---- a1-a8 in one call, HOST buffers (the e2e path) --------------------------------
+ * x_host: n x d vectors in host memory (pinned for full copy speed).  Copies x to the device, runs
+ * k-means (rank 0, seed kmeans_seed, 15 Lloyd steps, 256 samples per cluster) + N1, the
+ * partition (pp), every shard LPT-placed on this rank (bp; built, folded into the owner rows and
+ * reused), N2 and the final fold, then copies this rank's merged rows (ascending gid) to
+ * merged_host (capacity n x R; the first *n_owned_host rows are written) and their distances to
+ * merged_d_host (optional).  entry_host (optional) receives the global entry point (R13).
+ * comm: the communicator (NULL = world 1); collective over its ranks.  Synchronises.  Unlike the
+ * rest of the ABI this call allocates its device temporaries itself (stream-ordered, released
+ * before it returns). */
+sg_status scalegann_build_index_host(void* comm, const void* x_host, sg_dtype dtype, uint64_t n, uint32_t d,
+                                     const sg_partition_params* pp, const sg_build_params* bp,
+                                     uint64_t kmeans_seed, uint32_t* merged_host, float* merged_d_host,
+                                     uint64_t* n_owned_host, uint32_t* entry_host, void* stream);
+
 /* ---- a9: recall evaluation (reading R14) ------------------
  * Greedy best-first beam search from `entry` over graph (n x R global ids) for
  * nq queries (nq x d, same dtype as x); out_ids nq x topk.  Distances are P8's

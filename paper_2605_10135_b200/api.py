@@ -48,7 +48,8 @@ EXPORTS = [
     "scalegann_build_shard", "scalegann_optimize_from_knn", "scalegann_get_unique_id", "scalegann_comm_init",
     "scalegann_comm_destroy", "scalegann_comm_rank", "scalegann_broadcast_centroids", "scalegann_exchange_records",
     "scalegann_merge_plan_workspace", "scalegann_merge_plan", "scalegann_merge_init", "scalegann_merge_shard",
-    "scalegann_merge_finish", "scalegann_merge_workspace", "scalegann_merge", "scalegann_search_workspace",
+    "scalegann_merge_finish", "scalegann_merge_workspace", "scalegann_merge", "scalegann_build_index_host",
+    "scalegann_search_workspace",
     "scalegann_search_eval", "scalegann_search_shards_workspace", "scalegann_search_eval_shards", "scalegann_gemm_probe", "scalegann_stats_enable", "scalegann_stats_read", "scalegann_knn_profile",
 ]
 
@@ -105,6 +106,8 @@ def load(build_if_missing: bool = True):
                                    vp, vp, vp, vp, vp, vp], i32),
         "scalegann_merge_finish": ([u32, u32, vp, vp, u64, vp, vp, vp, sz, vp], i32),
         "scalegann_merge_workspace": ([vp, u64, u32, u32, P(i32), vp, u32, psz, pu64, vp], i32),
+        "scalegann_build_index_host": ([vp, vp, i32, u64, u32, P(PartitionParams), P(BuildParams), u64, vp, vp, pu64,
+                                        pu32, vp], i32),
         "scalegann_merge": ([vp, vp, u64, u32, u32, P(i32), P(vp), pu64, P(vp), P(vp), u32, vp, vp, pu64, vp, sz,
                              vp], i32),
         "scalegann_search_workspace": ([u64, u32, i32, u32, u32, u32, psz], i32),
@@ -457,6 +460,29 @@ def scalegann_merge(home, idmaps, graphs, graphs_d, owner=None, comm=None, ws=No
                              _ptr_array(graphs_d, k), R, _ptr(merged), _ptr(merged_d), ctypes.byref(no), p, nbytes,
                              _stream()))
     return merged, merged_d
+
+
+# ----------------------------------------------------------------------------- a1-a8, one call
+def scalegann_build_index_host(x_host, merged_host, comm=None, k=4, omega=2, epsilon=1.2, theta0_ppm=400_000,
+                               alpha=1.0, block_size=65536, capacity=0, L_=128, R=64, metric=SG_L2,
+                               precision=PREC_AUTO, prune_rule=0, protected_edges=0, kmeans_seed=42,
+                               merged_d_host=None):
+    """Whole build from host buffers: x_host (n x d, CPU, pinned for speed) in, this rank's merged
+    rows out into merged_host (CPU, capacity n x R).  Returns (n_owned, global entry)."""
+    L = load()
+    if x_host.is_cuda or merged_host.is_cuda or not x_host.is_contiguous() or not merged_host.is_contiguous():
+        raise ValueError("x_host and merged_host must be contiguous host tensors")
+    n, d = x_host.shape
+    if merged_host.numel() < n * R:
+        raise ValueError("merged_host needs room for n x R ids")
+    pp = PartitionParams(k, omega, epsilon, theta0_ppm, alpha, block_size, capacity)
+    bp = build_params(L_, R, metric, precision, prune_rule, protected_edges)
+    no = ctypes.c_uint64(0)
+    ent = ctypes.c_uint32(0)
+    _check(L.scalegann_build_index_host(comm, _ptr(x_host), _dtype(x_host), n, d, ctypes.byref(pp), ctypes.byref(bp),
+                                        kmeans_seed, _ptr(merged_host), _ptr(merged_d_host), ctypes.byref(no),
+                                        ctypes.byref(ent), _stream()))
+    return no.value, ent.value
 
 
 # ----------------------------------------------------------------------------- diagnostics

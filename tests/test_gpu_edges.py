@@ -121,3 +121,16 @@ def test_rerun_is_byte_identical(api, kind):
     a = build_index(x, cfg)
     b = build_index(x, cfg)
     assert torch.equal(a.home, b.home) and torch.equal(a.merged, b.merged) and torch.equal(a.merged_d, b.merged_d)
+
+
+def test_build_index_host_equals_pipeline(api):
+    """The one-call host-buffer entry point (bench's e2e path) builds the pipeline's graph."""
+    from paper_2605_10135_b200.pipeline import BuildConfig, build_index
+    x = datagen.sift_like(12_000, 64, seed=87)
+    cfg = BuildConfig(k=3, L=64, R=32)
+    ref = build_index(x.cuda(), cfg)
+    out = torch.empty(12_000 * 32, dtype=torch.int32).pin_memory()
+    outd = torch.empty(12_000 * 32, dtype=torch.float32).pin_memory()
+    no, entry = api.scalegann_build_index_host(x.pin_memory(), out, k=3, L_=64, R=32, merged_d_host=outd)
+    assert no == 12_000 and entry == ref.entry
+    assert torch.equal(out.view(-1, 32), ref.merged.cpu()) and torch.equal(outd.view(-1, 32), ref.merged_d.cpu())
