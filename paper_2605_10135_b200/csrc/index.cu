@@ -14,7 +14,22 @@ struct DevArena {   // stream-ordered device allocations freed together
     cudaStream_t st;
     void* ptrs[96];
     int n = 0;
-    explicit DevArena(cudaStream_t s) : st(s) {}
+    explicit DevArena(cudaStream_t s) : st(s) {
+        // keep freed blocks in the device's default pool between calls (the default release
+        // threshold of 0 would hand them back to the driver at every synchronisation, and the
+        // next call would map gigabytes again)
+        static bool once = false;
+        if (!once) {
+            int dev = 0;
+            cudaMemPool_t pool;
+            if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                uint64_t keep = ~0ull;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+            }
+            cudaGetLastError();
+            once = true;
+        }
+    }
     sg_status take(void** p, size_t bytes) {
         if (n == 96) { set_error("build_index: too many allocations"); return SG_ERR_INVALID_ARG; }
         SG_CUDA(cudaMallocAsync(p, bytes ? bytes : 256, st));
