@@ -28,7 +28,7 @@ template <uint32_t NB, uint32_t NBB>
 __device__ __forceinline__ uint32_t lookup(const uint4* bk, const uint2* br, const uint32_t* sk, const uint8_t* sr,
                                            uint32_t nstash, uint32_t b) {
     const uint32_t h = hslot(b, NBB);
-    const uint4 k0 = bk[2 * h], k1 = bk[2 * h + 1];
+    const uint4 k0 = bk[h], k1 = bk[NB + h];   // slots 0-3 and 4-7 in separate arrays: bank group h mod 8
     const uint2 rw = br[h];
     uint32_t r = 0xFFFFFFFFu;
     r = k0.x == b ? (rw.x & 0xFFu) : r;
@@ -92,7 +92,7 @@ struct PruneLayout {
     static constexpr uint32_t SR = al(SK + STASH * 4);
     static constexpr uint32_t NST = al(SR + STASH);
     static constexpr uint32_t BLOOM = al(NST + 16);
-    static constexpr uint32_t CNT = al(BLOOM + 128);
+    static constexpr uint32_t CNT = al(BLOOM + 256);
     static constexpr uint32_t NA = al(CNT + LP * 4);
     static constexpr uint32_t OFF = al(NA + LP * 4);
     static constexpr uint32_t STG = al(OFF + (LP + 1) * 4);
@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(PW * 32) prune_kernel(const uint32_t* __restri
     uint32_t* sk = (uint32_t*)(base + Lay::SK);        // stash keys
     uint8_t* sr = base + Lay::SR;                      // stash ranks
     uint32_t* nst = (uint32_t*)(base + Lay::NST);      // stash count
-    uint32_t* bloom = (uint32_t*)(base + Lay::BLOOM);  // 32 words
+    uint32_t* bloom = (uint32_t*)(base + Lay::BLOOM);  // 64 words
     uint32_t* cnt = (uint32_t*)(base + Lay::CNT);      // detour count per rank
     uint32_t* na = (uint32_t*)(base + Lay::NA);        // N[a]
     uint32_t* off = (uint32_t*)(base + Lay::OFF);      // counting-sort offsets per count value (L + 1)
@@ -135,15 +135,16 @@ __global__ void __launch_bounds__(PW * 32) prune_kernel(const uint32_t* __restri
         for (uint32_t r = lane; r < LP; r += 32) { na[r] = r < L ? Na[r] : SG_SENT; cnt[r] = 0; }
         for (uint32_t r = lane; r <= LP; r += 32) off[r] = 0;
         bloom[lane] = 0;
+        bloom[32 + lane] = 0;
         __syncwarp();
         for (uint32_t r = lane; r < L; r += 32) {
             const uint32_t id = na[r];
             if (id == SG_SENT) continue;
             const uint32_t h = hslot(id, NBB);
-            atomicOr(&bloom[(id >> 5) & 31u], 1u << (id & 31u));   // filter bit = id mod 1024
+            atomicOr(&bloom[(id >> 5) & 63u], 1u << (id & 31u));   // filter bit = id mod 2048
             const uint32_t slot = atomicAdd(&bfill[h], 1u);
             if (slot < 8) {
-                bkeys[h * 8 + slot] = id;
+                bkeys[(slot < 4 ? h * 4 : NB * 4 + h * 4 - 4) + slot] = id;
                 branks[h * 8 + slot] = (uint8_t)r;
             } else {
                 const uint32_t i = atomicAdd(nst, 1u);
@@ -152,7 +153,7 @@ __global__ void __launch_bounds__(PW * 32) prune_kernel(const uint32_t* __restri
         }
         __syncwarp();
         const uint32_t nstash = *nst;
-        const uint32_t fword = bloom[lane];   // 1024-bit membership filter, one word per lane
+        const uint32_t fword = bloom[lane], fword1 = bloom[32 + lane];   // 2048-bit filter, two words per lane
         if (nstash > STASH) {   // pathological hash clustering: exact but slow path (never observed)
             for (uint32_t r0 = 0; r0 < L; r0++) {
                 const uint32_t dl = na[r0];
@@ -183,7 +184,9 @@ __global__ void __launch_bounds__(PW * 32) prune_kernel(const uint32_t* __restri
 #pragma unroll
                         for (int q = 0; q < LPL; q++) {
                             const uint32_t b = bv[u][q];
-                            const uint32_t fw = __shfl_sync(0xffffffffu, fword, (b >> 5) & 31u);
+                            const uint32_t f0 = __shfl_sync(0xffffffffu, fword, (b >> 5) & 31u);
+                            const uint32_t f1 = __shfl_sync(0xffffffffu, fword1, (b >> 5) & 31u);
+                            const uint32_t fw = (b & 1024u) ? f1 : f0;
                             lm |= (__funnelshift_r(fw, fw, b) & 1u) << ((u - u0) * LPL + q);
                             stg[((u - u0) * LPL + q) * 32 + lane] = b;   // slot-major: conflict free
                         }
