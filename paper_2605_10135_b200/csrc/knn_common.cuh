@@ -161,6 +161,7 @@ struct KnnParams {
     // and recomputed by the fallback launch (alpha100 = 0: plain rank-L thresholds).
     uint32_t alpha100, beta;
     uint32_t eager;            // transposed kernel: compact a stream once it holds want + eager
+    uint32_t kshift;           // extrapolated compaction keeps <= want + ((C - ROOM - want) >> kshift)
     uint32_t* fail_count;      // device counter of rows to recompute (extrapolated launch)
     uint32_t* fail_rows;       // their operand rows
     const uint32_t* n_rows_dev;   // fallback launch: A row count read on the device (nullptr: ma)

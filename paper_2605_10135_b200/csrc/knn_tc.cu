@@ -270,7 +270,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 uint32_t want = want_full, kmax = kmax_full, trig = C - ROOM;
                 if (p.alpha100) {
                     const uint32_t rr = (uint32_t)(slope * (float)(ti + 1)) + p.beta;
-                    if (rr < want) { want = rr; kmax = want + (C - ROOM - want) / 8; }
+                    if (rr < want) { want = rr; kmax = want + ((C - ROOM - want) >> p.kshift); }
                     if (want + p.eager < trig) trig = want + p.eager;
                 }
                 // this stream's two 32-column passes.  One TMEM load each (18 warps leave 96
@@ -636,6 +636,8 @@ sg_status knn_core(const Operand& A, const Operand& B, int /*metric*/, bool self
     p.alpha100 = (uint32_t)alpha;
     p.beta = (uint32_t)(beta >= 0 ? beta : tr ? 6 : knn2_supported(A.nfull, L, false) ? 8 : 12);   // per column stream
     p.eager = (uint32_t)(eager >= 0 ? eager : tr ? 16 : 64);
+    static const int kshift = env_int("SG_KNN_KSHIFT", 3);   // in-loop compaction keeps want + room >> kshift
+    p.kshift = (uint32_t)(kshift >= 0 && kshift < 16 ? kshift : 3);
     p.fail_count = fail_count;
     p.fail_rows = fail_rows;
     SG_TRY(launch_knn(A, B, p, st));

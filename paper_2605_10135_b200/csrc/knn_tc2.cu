@@ -284,7 +284,7 @@ knn_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 uint32_t want = want_full, kmax = kmax_full, trig = C - ROOM2;
                 if (p.alpha100) {
                     const uint32_t rr = (uint32_t)(slope * (float)(ti + 1)) + p.beta;
-                    if (rr < want) { want = rr; kmax = want + (C - ROOM2 - want) / 8; }
+                    if (rr < want) { want = rr; kmax = want + ((C - ROOM2 - want) >> p.kshift); }
                     if (want + p.eager < trig) trig = want + p.eager;
                 }
                 uint32_t vv[32];
