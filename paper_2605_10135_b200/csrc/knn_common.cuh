@@ -162,6 +162,7 @@ struct KnnParams {
     uint32_t alpha100, beta;
     uint32_t eager;            // transposed kernel: compact a stream once it holds want + eager
     uint32_t kshift;           // extrapolated compaction keeps <= want + ((C - ROOM - want) >> kshift)
+    uint32_t z100;             // > 0: binomial extrapolated targets (z score x 100), else linear (alpha)
     uint32_t* fail_count;      // device counter of rows to recompute (extrapolated launch)
     uint32_t* fail_rows;       // their operand rows
     const uint32_t* n_rows_dev;   // fallback launch: A row count read on the device (nullptr: ma)

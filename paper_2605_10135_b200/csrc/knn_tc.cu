@@ -243,6 +243,9 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         const uint32_t nbar = NACC * 8 * 32;                 // active epilogue threads
         // extrapolated target rank per stream after tile ti: slope * (ti + 1) + beta
         const float slope = p.alpha100 * 0.005f * (float)p.L * (float)BN / (float)p.mb;
+        // binomial target (p.z100 > 0): after a fraction f of the columns a stream holds on average
+        // L f / 2 of the row's top-L, with variance L f / 2 (1 - f / 2)
+        const float fstep = (float)BN / (float)p.mb, mu_step = 0.5f * (float)p.L * fstep, zf = 0.01f * (float)p.z100;
         // the self column is inserted like any other (its key is the row's smallest) and removed
         // in the final phase; with plain rank-L thresholds it takes one of the kept ranks
         const uint32_t want_full = p.L + (p.self_exclude ? 1u : 0u);
@@ -269,7 +272,13 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 // the fraction of columns seen; trigger: buffer full, or `eager` above the target
                 uint32_t want = want_full, kmax = kmax_full, trig = C - ROOM;
                 if (p.alpha100) {
-                    const uint32_t rr = (uint32_t)(slope * (float)(ti + 1)) + p.beta;
+                    uint32_t rr;
+                    if (p.z100) {   // binomial target: mean + z sd of this stream's share of the top-L
+                        const float mu = mu_step * (float)(ti + 1), fr = fstep * (float)(ti + 1);
+                        rr = (uint32_t)(mu + zf * sqrtf(mu * fmaxf(1.f - 0.5f * fr, 0.f))) + p.beta;
+                    } else {
+                        rr = (uint32_t)(slope * (float)(ti + 1)) + p.beta;
+                    }
                     if (rr < want) { want = rr; kmax = want + ((C - ROOM - want) >> p.kshift); }
                     if (want + p.eager < trig) trig = want + p.eager;
                 }
@@ -636,6 +645,8 @@ sg_status knn_core(const Operand& A, const Operand& B, int /*metric*/, bool self
     p.alpha100 = (uint32_t)alpha;
     p.beta = (uint32_t)(beta >= 0 ? beta : tr ? 6 : knn2_supported(A.nfull, L, false) ? 8 : 12);   // per column stream
     p.eager = (uint32_t)(eager >= 0 ? eager : tr ? 16 : 64);
+    static const int z100 = env_int("SG_KNN_Z", 0);   // binomial thresholds: z score x 100 (0 = linear)
+    p.z100 = (uint32_t)(z100 > 0 ? z100 : 0);
     static const int kshift = env_int("SG_KNN_KSHIFT", 3);   // in-loop compaction keeps want + room >> kshift
     p.kshift = (uint32_t)(kshift >= 0 && kshift < 16 ? kshift : 3);
     p.fail_count = fail_count;
