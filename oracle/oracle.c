@@ -18,6 +18,8 @@
  *                              k=1 -> mean, k=#distinct -> 0 distortion,
  *                              non-increasing distortion.  Not in the bit-exact
  *                              chain (centroids are an input to partition).
+ *   oracle_kmeans_distortion  the sample distortion that judges the GPU
+ *                              k-means (R0); pinned by hand values on a line.
  *   oracle_centroid_dist   P1  fixed fp32 fmaf chain (reading R1).  Pinned by
  *                              exact small-integer cases.
  *   oracle_partition       P2/P3  blockwise-adaptive primaries + Algorithm 1
@@ -33,7 +35,11 @@
  *                              tests/golden/prune_reverse_example.json and
  *                              invariants only.
  *   oracle_reverse         P6  reverse-edge insertion.  PARITY UNPINNED BY THE
- *                              PAPER (same reason); hand example + invariants.
+ *                              PAPER (same reason); hand example + invariants,
+ *                              and a second hand example where the (k, x) cap
+ *                              order of rev[] decides the output
+ *                              (tests/golden/reverse_order_example.json;
+ *                              oracle_reverse_lists exposes rev[]).
  *   oracle_merge           P7  edge union + re-prune.  Pinned
  *                              by single-shard identity and the {a,b}u{b,c}
  *                              example, truncation optimality.
