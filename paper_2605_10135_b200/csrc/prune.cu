@@ -1,8 +1,9 @@
 // a6 — rank-based detour-count prune (north_star stage 3; reading R10, CAGRA prior art).
 //
-// One warp per node a.  N[a] (L ids) goes into a shared-memory bucketized table id -> rank
-// (L/2 buckets of 8 slots + stash: a lookup is two 16-byte loads and 8 compares, no probing).  For each rank r_ad the warp reads the 2-hop row N[delta] (delta = N[a][r_ad])
-// with coalesced 16-byte loads (4 rows in flight per lane batch) and, for every b in it that
+// One warp per node a.  N[a] (L ids) goes into a shared-memory cuckoo table id -> rank (two
+// 8-byte loads and two compares per lookup) and a 2048-bit register filter.  For each rank r_ad
+// the warp reads the 2-hop row N[delta] (delta = N[a][r_ad]) with one vector load per row
+// (4 rows in flight per lane batch) and, for every b in it that
 // is also in N[a] at rank r_ab with max(r_ad, r_db) < r_ab (rule P; rule 1: r_ad < r_ab),
 // increments cnt[r_ab] in shared memory.  The ranks are then ordered stably by (cnt, rank)
 // (sentinel ranks last) with a counting sort and the first R written with their kNN distances.
@@ -15,34 +16,26 @@ namespace sg {
 namespace {
 
 
-__device__ __forceinline__ uint32_t hslot(uint32_t id, uint32_t bits) { return (id * 0x9E3779B1u) >> (32 - bits); }
 
 // Membership table of N[a]: NB = LP/2 buckets of 8 slots (keys u32, ranks u8), one hash; a
 // lookup reads the whole bucket with two 16-byte loads and compares 8 keys, with no probe loop (a
 // probing table makes every lane wait for the warp's longest chain).  Keys that find their
 // bucket full go to a small stash, scanned only when it is not empty (warp-uniform).
-constexpr uint32_t STASH = 32;
-constexpr uint32_t EMPTY = 0xFFFFFFFEu;   // empty slot: no id (< 2^31) and not SENT, so never matched
+constexpr uint32_t STASH = 32;   // *nst > STASH flags a node whose table insertion did not settle
 
-template <uint32_t NB, uint32_t NBB>
-__device__ __forceinline__ uint32_t lookup(const uint4* bk, const uint2* br, const uint32_t* sk, const uint8_t* sr,
-                                           uint32_t nstash, uint32_t b) {
-    const uint32_t h = hslot(b, NBB);
-    const uint4 k0 = bk[h], k1 = bk[NB + h];   // slots 0-3 and 4-7 in separate arrays: bank group h mod 8
-    const uint2 rw = br[h];
-    uint32_t r = 0xFFFFFFFFu;
-    r = k0.x == b ? (rw.x & 0xFFu) : r;
-    r = k0.y == b ? ((rw.x >> 8) & 0xFFu) : r;
-    r = k0.z == b ? ((rw.x >> 16) & 0xFFu) : r;
-    r = k0.w == b ? (rw.x >> 24) : r;
-    r = k1.x == b ? (rw.y & 0xFFu) : r;
-    r = k1.y == b ? ((rw.y >> 8) & 0xFFu) : r;
-    r = k1.z == b ? ((rw.y >> 16) & 0xFFu) : r;
-    r = k1.w == b ? (rw.y >> 24) : r;
-    if (nstash) {
-        for (uint32_t i = 0; i < nstash; i++) r = sk[i] == b ? sr[i] : r;
-    }
-    return r;
+// Cuckoo table of N[a]: 8 NB = 4 L_pad slots of (id << 32 | rank), two hashes; a lookup reads
+// both candidate slots (two 8-byte loads, two compares, no probe loop).  Parallel insertion
+// (atomicExch, evicted entries move to their other slot) at load 1/4; a node whose insertion
+// does not settle takes the exact slow path.
+__device__ __forceinline__ uint32_t ch1(uint32_t id, uint32_t bits) { return (id * 0x9E3779B1u) >> (32 - bits); }
+__device__ __forceinline__ uint32_t ch2(uint32_t id, uint32_t bits) {
+    const uint32_t h = ((id ^ (id >> 16)) * 0x85EBCA6Bu) >> (32 - bits);
+    return h == ch1(id, bits) ? h ^ 1u : h;
+}
+__device__ __forceinline__ uint32_t lookup(const uint64_t* tab, uint32_t bits, uint32_t b) {
+    const uint64_t e1 = tab[ch1(b, bits)], e2 = tab[ch2(b, bits)];
+    // an empty slot holds ~0: its low word is "no rank", so a SENT id (never inserted) misses
+    return (uint32_t)(e1 >> 32) == b ? (uint32_t)e1 : (uint32_t)(e2 >> 32) == b ? (uint32_t)e2 : 0xFFFFFFFFu;
 }
 
 constexpr uint32_t QCAP = 256;   // lookup queue entries per warp (flushed every 256 / (32 LPL) rows)
@@ -85,12 +78,8 @@ struct PruneLayout {
     static constexpr uint32_t LP = LPL * 32, NB = LP / 2;
     static constexpr int FLUSH = QCAP / (32 * LPL) < 4 ? QCAP / (32 * LPL) : 4;
     static constexpr uint32_t al(size_t v) { return (uint32_t)((v + 15) / 16 * 16); }
-    static constexpr uint32_t BKEYS = 0;
-    static constexpr uint32_t BRANKS = al(BKEYS + NB * 32);
-    static constexpr uint32_t BFILL = al(BRANKS + NB * 8);
-    static constexpr uint32_t SK = al(BFILL + NB * 4);
-    static constexpr uint32_t SR = al(SK + STASH * 4);
-    static constexpr uint32_t NST = al(SR + STASH);
+    static constexpr uint32_t BKEYS = 0;                  // cuckoo table: 8 NB slots of 8 bytes
+    static constexpr uint32_t NST = al(BKEYS + NB * 64);
     static constexpr uint32_t BLOOM = al(NST + 16);
     static constexpr uint32_t CNT = al(BLOOM + 256);
     static constexpr uint32_t NA = al(CNT + LP * 4);
@@ -114,11 +103,8 @@ __global__ void __launch_bounds__(PW * 32) prune_kernel(const uint32_t* __restri
     const uint32_t lt = (1u << lane) - 1u;
     using Lay = PruneLayout<LPL>;
     uint8_t* base = sm + (size_t)w * Lay::PER;
-    uint32_t* bkeys = (uint32_t*)(base + Lay::BKEYS);  // [NB][8]
-    uint8_t* branks = base + Lay::BRANKS;              // [NB][8]
-    uint32_t* bfill = (uint32_t*)(base + Lay::BFILL);  // [NB]
-    uint32_t* sk = (uint32_t*)(base + Lay::SK);        // stash keys
-    uint8_t* sr = base + Lay::SR;                      // stash ranks
+    uint64_t* tab = (uint64_t*)(base + Lay::BKEYS);    // [8 NB] cuckoo slots (id << 32 | rank)
+    constexpr uint32_t TBITS = NBB + 3;
     uint32_t* nst = (uint32_t*)(base + Lay::NST);      // stash count
     uint32_t* bloom = (uint32_t*)(base + Lay::BLOOM);  // 64 words
     uint32_t* cnt = (uint32_t*)(base + Lay::CNT);      // detour count per rank
@@ -129,8 +115,7 @@ __global__ void __launch_bounds__(PW * 32) prune_kernel(const uint32_t* __restri
     const uint64_t nwarps = (uint64_t)gridDim.x * PW;
     for (uint64_t a = (uint64_t)blockIdx.x * PW + w; a < m; a += nwarps) {
         const uint32_t* Na = knn + a * L;
-        for (uint32_t i = lane; i < NB * 8; i += 32) bkeys[i] = EMPTY;
-        for (uint32_t i = lane; i < NB; i += 32) bfill[i] = 0;
+        for (uint32_t i = lane; i < NB * 8; i += 32) tab[i] = ~0ull;
         if (lane == 0) *nst = 0;
         for (uint32_t r = lane; r < LP; r += 32) { na[r] = r < L ? Na[r] : SG_SENT; cnt[r] = 0; }
         for (uint32_t r = lane; r <= LP; r += 32) off[r] = 0;
@@ -140,21 +125,23 @@ __global__ void __launch_bounds__(PW * 32) prune_kernel(const uint32_t* __restri
         for (uint32_t r = lane; r < L; r += 32) {
             const uint32_t id = na[r];
             if (id == SG_SENT) continue;
-            const uint32_t h = hslot(id, NBB);
             atomicOr(&bloom[(id >> 5) & 63u], 1u << (id & 31u));   // filter bit = id mod 2048
-            const uint32_t slot = atomicAdd(&bfill[h], 1u);
-            if (slot < 8) {
-                bkeys[(slot < 4 ? h * 4 : NB * 4 + h * 4 - 4) + slot] = id;
-                branks[h * 8 + slot] = (uint8_t)r;
-            } else {
-                const uint32_t i = atomicAdd(nst, 1u);
-                if (i < STASH) { sk[i] = id; sr[i] = (uint8_t)r; }
+            uint64_t e = ((uint64_t)id << 32) | r;
+            uint32_t slot = ch1(id, TBITS);
+            uint32_t it = 0;
+            for (; it < 64; it++) {
+                const uint64_t old = atomicExch((unsigned long long*)&tab[slot], (unsigned long long)e);
+                if (old == ~0ull) break;
+                e = old;   // evicted: move it to its other slot
+                const uint32_t oid = (uint32_t)(old >> 32), a1 = ch1(oid, TBITS);
+                slot = slot == a1 ? ch2(oid, TBITS) : a1;
             }
+            if (it == 64) atomicExch(nst, STASH + 1);   // did not settle: the node takes the slow path
         }
         __syncwarp();
         const uint32_t nstash = *nst;
         const uint32_t fword = bloom[lane], fword1 = bloom[32 + lane];   // 2048-bit filter, two words per lane
-        if (nstash > STASH) {   // pathological hash clustering: exact but slow path (never observed)
+        if (nstash > STASH) {   // cuckoo insertion did not settle: exact but slow path
             for (uint32_t r0 = 0; r0 < L; r0++) {
                 const uint32_t dl = na[r0];
                 if (dl == SG_SENT) continue;
@@ -217,7 +204,7 @@ __global__ void __launch_bounds__(PW * 32) prune_kernel(const uint32_t* __restri
                     for (uint32_t i = lane; i < ((rule & 0x100u) ? 0u : total); i += 32) {   // 0x100: no lookups
                         const uint64_t e = qe[i];
                         const uint32_t b = (uint32_t)e;
-                        const uint32_t r_ab = lookup<NB, NBB>((const uint4*)bkeys, (const uint2*)branks, sk, sr, nstash, b);
+                        const uint32_t r_ab = lookup(tab, TBITS, b);
                         if (r_ab != 0xFFFFFFFFu && (uint32_t)(e >> 32) < r_ab) atomicAdd(&cnt[r_ab], 1u);
                     }
                     __syncwarp();
